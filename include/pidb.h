@@ -1,0 +1,190 @@
+/*
+ * pidb.h — C ABI of the B200-native (sm_100a) depth hot path for
+ * Probabilistic Inclusion Depth (PID), PID-mean and eID.
+ *
+ * The reference package `fuzzdepth` is pure Python/numpy; its "operator API"
+ * is the set of Python functions listed per entry point below.  A ctypes
+ * binding of exactly these symbols is what the reference would need to route
+ * its hot path here; the Python mirror in
+ * paper_2512_15187_b200/ is that binding.
+ *
+ * Conventions (all entry points):
+ *   - stream-ordered: every call enqueues work on `stream` (a cudaStream_t,
+ *     passed as void* so this header needs no CUDA include) and returns without
+ *     synchronising, except where stated;
+ *   - pointers are caller-owned DEVICE pointers unless stated; nothing here
+ *     allocates device memory except through caller-provided workspaces;
+ *   - member data is row-major (n rows = members, m columns = cells), row
+ *     stride `ld` elements; ld*sizeof(elem) must be a multiple of 16 bytes and
+ *     the base pointer 16-byte aligned (TMA requirement);
+ *   - dtype is PIDB_F32 or PIDB_F64 (the reference keeps float64 members in
+ *     float64, /root/reference/pkg/src/fuzzdepth/grid.py:103-104);
+ *   - weights `w` are per-cell float64 (nullable = uniform unit weights,
+ *     /root/reference/pkg/src/fuzzdepth/grid.py:39-57);
+ *   - return 0 on success, a negative PIDB_E* code otherwise; the message is
+ *     available from pidb_last_error() (thread-local).
+ */
+#ifndef PIDB_H
+#define PIDB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PIDB_ABI_VERSION 1
+
+enum pidb_status {
+  PIDB_OK = 0,
+  PIDB_EINVAL = -1,      /* bad argument (maps to ValidationError)            */
+  PIDB_ECUDA = -2,       /* CUDA runtime / launch failure                      */
+  PIDB_EUNSUPPORTED = -3,/* shape outside what the kernels support             */
+  PIDB_EWORKSPACE = -4   /* workspace too small                                */
+};
+
+enum pidb_dtype { PIDB_F32 = 0, PIDB_F64 = 1 };
+
+/* Epilogue modes for pidb_depth_epilogue. */
+enum pidb_epilogue_mode {
+  PIDB_EPI_PID_MEAN = 0, /* /root/reference/pkg/src/fuzzdepth/depth.py:274-279 */
+  PIDB_EPI_PID = 1       /* /root/reference/pkg/src/fuzzdepth/depth.py:226-227 */
+};
+
+int pidb_abi_version(void);
+const char* pidb_last_error(void);
+
+/* ---------------------------------------------------------------- K5 ----
+ * PID-mean partial sums in ONE streaming pass over the member matrix.
+ * Replaces mean_mask (grid.py:251-261) + mask_mass(mean) (grid.py:242-244,
+ * depth.py:264) + _member_mean_terms (depth.py:231-243) as used by
+ * depth_pid_mean (depth.py:246-287).
+ *   row_plain[i] = sum_x w(x) u_i(x) S(x),  S(x) = sum_j u_j(x)
+ *                  (= N * num_i of depth.py:274, = sum_j G[i,j] of depth.py:156)
+ *   mass[i]      = sum_x w(x) u_i(x)                     (depth.py:275)
+ *   col_mean[0]  = sum_x w(x) S(x)     (= N * mean_mass_total, depth.py:264)
+ * Outputs are additive over disjoint cell shards (multi-GPU: allreduce-sum).
+ * Deterministic: fixed reduction order for a fixed device. */
+size_t pidb_pid_mean_workspace_bytes(int64_t n, int64_t m, int dtype);
+int pidb_pid_mean_partials(const void* u, int dtype, int64_t n, int64_t m,
+                           int64_t ld, const double* w, double* row_plain,
+                           double* mass, double* col_mean, void* ws,
+                           size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- K9 ----
+ * Second pass of the exact linear-time PID (certifier / product path):
+ *   col_inv[j] = sum_x w(x) u_j(x) T(x),  T(x) = sum_i inv[i] u_i(x)
+ * which equals sum_i inv[i] G[i,j] of _pairwise_sums (depth.py:157,160).
+ * `inv` is a device array of n doubles (depth.py:164-168).  Additive over
+ * cell shards. */
+int pidb_pid_colsums(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                     const double* w, const double* inv, double* col_inv,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- K6/K7 -
+ * Member masses (member_masses, depth.py:88-102 -> weighted_sum,
+ * reduction.py:36-44) and, per member, the number of cells that are neither
+ * 0 nor 1 (ProbMask.is_binary, grid.py:125-127).  nonbinary may be NULL. */
+int pidb_member_masses(const void* u, int dtype, int64_t n, int64_t m,
+                       int64_t ld, const double* w, double* mass,
+                       int64_t* nonbinary, void* ws, size_t ws_bytes,
+                       void* stream);
+
+/* ---------------------------------------------------------------- K7 ----
+ * Pack 0/1 members to uint8 rows (ldb bytes, multiple of 16, zero padded up
+ * to ldb) for the integer Gram.  Values other than 0/1 are counted in
+ * nonbinary[i] (may be NULL) and packed as (u != 0). */
+int pidb_binary_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                     uint8_t* b, int64_t ldb, int64_t* nonbinary, void* stream);
+
+/* ---------------------------------------------------------------- K2 ----
+ * Exact integer intersection Gram on tcgen05 (kind::i8, int32 TMEM
+ * accumulators, int64 flush): I[i*n+j] = sum_x b_i(x) b_j(x), full n x n.
+ * Replaces gram_block(..., complement_cols=True) (reduction.py:75-97) as used
+ * by depth_eid (depth.py:192-210): |A_i \ A_j| = I[i,i] - I[i,j]. */
+size_t pidb_gram_i8_workspace_bytes(int64_t n, int64_t m);
+int pidb_gram_i8(const uint8_t* b, int64_t n, int64_t m, int64_t ldb,
+                 int64_t* gram, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- K1 ----
+ * Weighted Gram G[i*n+j] = sum_x w(x) u_i(x) u_j(x) in fp64 from 3xTF32
+ * tcgen05 MMAs (hi/lo split, fp32 TMEM accumulators flushed to fp64 every
+ * <=512 cells).  Replaces gram_block (reduction.py:75-97) as used by
+ * depth_pid/_pairwise_sums (depth.py:122-161, 213-228).  Float32 members only. */
+size_t pidb_gram_tf32x3_workspace_bytes(int64_t n, int64_t m);
+int pidb_gram_tf32x3(const float* u, int64_t n, int64_t m, int64_t ld,
+                     const double* w, double* gram, void* ws, size_t ws_bytes,
+                     void* stream);
+
+/* ---------------------------------------------------------------- K4 ----
+ * Gram -> (row_plain, col_inv): row_plain[i] = sum_j G[i,j],
+ * col_inv[j] = sum_i inv[i] G[i,j]  (depth.py:155-160). */
+int pidb_gram_reduce(const double* gram, int64_t n, const double* inv,
+                     double* row_plain, double* col_inv, void* stream);
+
+/* Depth epilogue: inverse masses (depth.py:164-168), in_in/in_out
+ * (mode-specific, see enum), depth = min(in_in, in_out) (depth.py:179) and
+ * ranks (stable, descending, ties by index; depth.py:80-85).
+ *   mode PID_MEAN: aux = col_mean (1 double), a = row_plain
+ *   mode PID     : aux = col_inv  (n doubles), a = row_plain
+ * `inv` (n doubles) is written with the inverse masses. */
+int pidb_depth_epilogue(int mode, int64_t n, const double* a,
+                        const double* mass, const double* aux, double* inv,
+                        double* in_in, double* in_out, double* depth,
+                        int64_t* rank, void* stream);
+
+/* Inverse masses alone (depth.py:164-168). */
+int pidb_inverse_masses(int64_t n, const double* mass, double* inv, void* stream);
+
+/* eID exact epilogue from the integer Gram (unit weights): per pair
+ * term = 1.0 - (double)(I[i,i]-I[i,j]) / (double)I[i,i]  (0 if I[i,i]==0),
+ * row/col sums exactly rounded (128-bit fixed point == math.fsum), then / n.
+ * Bit-identical to ref_eid (/root/reference/pkg/tests/reference_impl.py:60-70). */
+int pidb_eid_exact_epilogue(const int64_t* gram, int64_t n, double* in_in,
+                            double* in_out, double* depth, int64_t* rank,
+                            void* stream);
+
+/* eID epilogue from factorised sums (weighted binary ensembles):
+ * row_excess = n*m_i - row_plain[i], col excess = n_pos - col_inv[j], then
+ * in_in/in_out exactly as depth_eid (depth.py:203-209).  Not bit-exact (the
+ * reference itself is not); used when weights are present. */
+int pidb_eid_factorized_epilogue(int64_t n, const double* row_plain,
+                                 const double* mass, const double* col_inv,
+                                 double n_pos, double* inv, double* in_in,
+                                 double* in_out, double* depth, int64_t* rank,
+                                 void* stream);
+
+/* Ranks alone: stable descending order, ties by index (depth.py:80-85). */
+int pidb_ranks(int64_t n, const double* depth, int64_t* rank, void* stream);
+
+/* Materialised ensemble mean mask (grid.py:251-261): out[x] = (sum_i u_i(x))/n
+ * accumulated in fp64 in member order, i.e. bit-identical to the reference.
+ * (The depth kernels never materialise it; this serves the mean_mask API.) */
+int pidb_mean_mask(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                   double* out, void* stream);
+
+/* ---------------------------------------------------------------- K8 ----
+ * prob_inclusion (inclusion.py:22-40): out[0] = sum w u v, out[1] = sum w u.
+ * subset_epsilon (inclusion.py:43-64) on 0/1 data: out[0] = sum w a (1-b),
+ * out[1] = sum w a.  Additive over cell shards.  Synchronous (returns after
+ * the sums are in `out`, a HOST pointer to 2 doubles). */
+int pidb_pair_sums(const void* u, const void* v, int dtype, int64_t m,
+                   const double* w, int complement, double* out_host,
+                   void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- synth --
+ * Device-side synthetic ensembles (benchmark/test infrastructure; the
+ * per-member parameters are drawn on the host with the reference's Philox
+ * streams, synth.py:20-22).  params: n x 6 doubles
+ * (cy, cx, cz, ay, ax, az) for ellipsoids (synth.py:138-162), n x 3
+ * (cy, cx, radius) for disks (synth.py:30-51). */
+int pidb_synth_ellipsoids(float* out, int64_t n, int64_t res, int64_t ld,
+                          const double* params, double sigma, void* stream);
+int pidb_synth_disks(float* out, int64_t n, int64_t res, int64_t ld,
+                     const double* params, double sigma2, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIDB_H */

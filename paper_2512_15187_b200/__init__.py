@@ -1,0 +1,86 @@
+"""B200-native (sm_100a) Probabilistic Inclusion Depth — drop-in for the depth
+hot path of the reference package ``fuzzdepth`` (arXiv 2512.15187).
+
+Same entry points as the reference (depth_pid, depth_pid_mean, depth_eid,
+depth_by_method, prob_inclusion, subset_epsilon, member_masses, mean_mask,
+mask_mass, DepthResult, ranks_from_depths, and the GridSpec / ProbMask /
+BinaryMask / Ensemble containers); the arithmetic runs in hand-written CUDA
+kernels in ``libpidb.so`` (C ABI: include/pidb.h).  No CPU fallback.
+"""
+from .depth import (
+    CV_WARN_THRESHOLD,
+    METHOD_NAMES,
+    TILE_BYTES,
+    DepthResult,
+    depth_by_method,
+    depth_eid,
+    depth_pid,
+    depth_pid_mean,
+    mass_cv,
+    member_masses,
+    ranks_from_depths,
+    resolve_workers,
+)
+from .device import DeviceEnsemble, shard_bounds, stage
+from .errors import (
+    DegenerateEnsembleError,
+    FuzzdepthError,
+    GridMismatchError,
+    ManifestError,
+    ValidationError,
+    VolumeFormatError,
+)
+from .grid import (
+    BinaryMask,
+    Ensemble,
+    GridSpec,
+    ProbMask,
+    binarize,
+    binarize_ensemble,
+    binary_mass,
+    mask_mass,
+    mean_mask,
+    permute_cells,
+)
+from .inclusion import prob_inclusion, subset_epsilon
+from .reduction import gram_block
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BinaryMask",
+    "CV_WARN_THRESHOLD",
+    "DegenerateEnsembleError",
+    "DepthResult",
+    "DeviceEnsemble",
+    "Ensemble",
+    "FuzzdepthError",
+    "GridMismatchError",
+    "GridSpec",
+    "ManifestError",
+    "METHOD_NAMES",
+    "ProbMask",
+    "TILE_BYTES",
+    "ValidationError",
+    "VolumeFormatError",
+    "binarize",
+    "binarize_ensemble",
+    "binary_mass",
+    "depth_by_method",
+    "depth_eid",
+    "depth_pid",
+    "depth_pid_mean",
+    "gram_block",
+    "mask_mass",
+    "mass_cv",
+    "mean_mask",
+    "member_masses",
+    "permute_cells",
+    "prob_inclusion",
+    "ranks_from_depths",
+    "resolve_workers",
+    "shard_bounds",
+    "stage",
+    "subset_epsilon",
+    "__version__",
+]

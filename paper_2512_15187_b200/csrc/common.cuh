@@ -1,0 +1,117 @@
+// Shared device/host helpers for the sm_100a depth kernels: error plumbing,
+// mbarrier + TMA (cp.async.bulk.tensor) PTX wrappers, 128B-swizzle addressing,
+// warp reductions.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/pidb.h"
+
+namespace pidb {
+
+// ------------------------------------------------------------------ host ----
+void set_error(const char* fmt, ...);
+int check_cuda(cudaError_t e, const char* what);
+#define PIDB_REQUIRE(cond, ...)            \
+  do {                                     \
+    if (!(cond)) {                         \
+      ::pidb::set_error(__VA_ARGS__);      \
+      return PIDB_EINVAL;                  \
+    }                                      \
+  } while (0)
+#define PIDB_CUDA(call)                                        \
+  do {                                                         \
+    int _rc = ::pidb::check_cuda((call), #call);               \
+    if (_rc != PIDB_OK) return _rc;                            \
+  } while (0)
+#define PIDB_LAUNCH_CHECK(what) PIDB_CUDA(cudaGetLastError())
+
+int sm_count();
+int encode_tma_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
+                  uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                  uint32_t box_inner, uint32_t box_outer,
+                  CUtensorMapSwizzle swz);
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------- device ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 2D TMA tile load global -> shared, completion on an mbarrier (tx bytes).
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int32_t c0,
+                                            int32_t c1, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void prefetch_tma_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// Byte offset of logical 16B chunk `chunk` of 128-byte line `line` inside a
+// 1024B-aligned tile written by TMA with CU_TENSOR_MAP_SWIZZLE_128B.
+__device__ __forceinline__ uint32_t swz128(uint32_t line, uint32_t chunk) {
+  return (line << 7) | (((chunk ^ line) & 7u) << 4);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Error-free Fast2Sum accumulation: valid because s >= 1 >= x for masks
+// values in [0, 1] once s is seeded with 1.0 (the seed is removed in fp64).
+__device__ __forceinline__ void fast2sum_acc(float& s, float& c, float x) {
+  float t = __fadd_rn(s, x);
+  float z = __fsub_rn(t, s);
+  c = __fadd_rn(c, __fsub_rn(x, z));
+  s = t;
+}
+
+}  // namespace pidb

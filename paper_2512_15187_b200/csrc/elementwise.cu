@@ -1,0 +1,254 @@
+// K7 binary check/pack, K8 pair sums (prob_inclusion / subset_epsilon) and the
+// device-side synthetic ensembles used by the benchmark and GPU tests.
+//
+// Reference: prob_inclusion   /root/reference/pkg/src/fuzzdepth/inclusion.py:22-40
+//            subset_epsilon   /root/reference/pkg/src/fuzzdepth/inclusion.py:43-64
+//            ProbMask.is_binary /root/reference/pkg/src/fuzzdepth/grid.py:125-127
+//            _fuzzy_ellipsoid /root/reference/pkg/src/fuzzdepth/synth.py:138-162
+//            gen_fuzzy_disk   /root/reference/pkg/src/fuzzdepth/synth.py:30-51
+#include "common.cuh"
+
+namespace pidb {
+namespace {
+
+// ------------------------------------------------------------------ K7 ------
+// One warp per (member, 512-cell segment); 16-byte loads, 4-byte packed stores.
+template <typename T>
+__global__ void binary_pack_kernel(const T* __restrict__ u, int64_t n, int64_t m, int64_t ld,
+                                   uint8_t* __restrict__ b, int64_t ldb,
+                                   unsigned long long* __restrict__ nonbinary) {
+  const int64_t segs = (ldb + 511) / 512;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t job = wid; job < n * segs; job += nw) {
+    const int64_t i = job / segs;
+    const int64_t x0 = (job - i * segs) * 512 + lane * 16;
+    const T* row = u + i * ld;
+    unsigned long long bad = 0;
+    uint32_t packed[4] = {0, 0, 0, 0};
+    T vals[16];
+    if (x0 + 16 <= m) {  // 16-byte vector loads (rows are 16-byte aligned)
+      constexpr int PER = 16 / sizeof(T);
+#pragma unroll
+      for (int k = 0; k < 16 / PER; ++k) {
+        const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(row + x0) + k);
+        const T* t = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+        for (int e = 0; e < PER; ++e) vals[k * PER + e] = t[e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) vals[e] = x0 + e < m ? row[x0 + e] : T(0);
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const T v = vals[e];
+      bad += !(v == T(0) || v == T(1));
+      packed[e >> 2] |= (uint32_t)(v != T(0)) << (8 * (e & 3));
+    }
+    if (x0 < ldb) *reinterpret_cast<uint4*>(b + i * ldb + x0) =
+        make_uint4(packed[0], packed[1], packed[2], packed[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if (lane == 0 && bad && nonbinary) atomicAdd(&nonbinary[i], bad);
+  }
+}
+
+// ------------------------------------------------------------------ K8 ------
+template <typename T>
+__global__ void pair_sums_kernel(const T* __restrict__ u, const T* __restrict__ v, int64_t m,
+                                 const double* __restrict__ w, int complement,
+                                 double* __restrict__ part) {
+  double num = 0.0, den = 0.0;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    double a = (double)u[x];
+    const double bv = (double)v[x];
+    if (w) a *= w[x];
+    num = fma(a, complement ? (bv != 0.0 ? 0.0 : 1.0) : bv, num);
+    den += a;
+  }
+  __shared__ double s[2][32];
+  num = warp_sum(num);
+  den = warp_sum(den);
+  if ((threadIdx.x & 31) == 0) { s[0][threadIdx.x >> 5] = num; s[1][threadIdx.x >> 5] = den; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < (int)(blockDim.x / 32); ++k) { a += s[0][k]; b += s[1][k]; }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+__global__ void pair_finish_kernel(const double* __restrict__ part, int nb, double* out) {
+  double a = 0.0, b = 0.0;
+  for (int k = threadIdx.x; k < nb; k += 32) { a += part[2 * k]; b += part[2 * k + 1]; }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (threadIdx.x == 0) { out[0] = a; out[1] = b; }
+}
+
+// ---------------------------------------------------------------- synth -----
+// u = 1 inside the ellipsoid (rho <= 1), exp(-d^2/(2 sigma^2)) outside with
+// d = r (1 - 1/rho); evaluated in fp64 and rounded to fp32 like the reference.
+__global__ void synth_ellipsoids_kernel(float* __restrict__ out, int64_t n, int64_t res,
+                                        int64_t ld, const double* __restrict__ prm,
+                                        double sigma) {
+  const int64_t cells = res * res * res;
+  const int64_t i = blockIdx.y;
+  const double cy = prm[6 * i], cx = prm[6 * i + 1], cz = prm[6 * i + 2];
+  const double ay = prm[6 * i + 3], ax = prm[6 * i + 4], az = prm[6 * i + 5];
+  const double two_s2 = __dmul_rn(__dmul_rn(2.0, sigma), sigma);
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ld;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    float val = 0.0f;
+    if (c < cells) {
+      const int64_t y = c / (res * res), rem = c - y * res * res;
+      const int64_t x = rem / res, z = rem - x * res;
+      const double dy = (double)y - cy, dx = (double)x - cx, dz = (double)z - cz;
+      // explicit _rn intrinsics: no FMA contraction, same rounding as numpy
+      const double qy = __ddiv_rn(dy, ay), qx = __ddiv_rn(dx, ax), qz = __ddiv_rn(dz, az);
+      const double rho2 =
+          __dadd_rn(__dadd_rn(__dmul_rn(qy, qy), __dmul_rn(qx, qx)), __dmul_rn(qz, qz));
+      const double rho = __dsqrt_rn(rho2);
+      if (rho > 1.0) {
+        const double r2 =
+            __dadd_rn(__dadd_rn(__dmul_rn(dy, dy), __dmul_rn(dx, dx)), __dmul_rn(dz, dz));
+        const double d = __dmul_rn(__dsqrt_rn(r2), __dsub_rn(1.0, __ddiv_rn(1.0, rho)));
+        val = (float)exp(__ddiv_rn(-__dmul_rn(d, d), two_s2));
+      } else {
+        val = 1.0f;
+      }
+    }
+    out[i * ld + c] = val;
+  }
+}
+
+__global__ void synth_disks_kernel(float* __restrict__ out, int64_t n, int64_t res, int64_t ld,
+                                   const double* __restrict__ prm, double sigma2) {
+  const int64_t cells = res * res;
+  const int64_t i = blockIdx.y;
+  const double cy = prm[3 * i], cx = prm[3 * i + 1], radius = prm[3 * i + 2];
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ld;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    float val = 0.0f;
+    if (c < cells) {
+      const int64_t y = c / res, x = c - y * res;
+      const double dy = (double)y - cy, dx = (double)x - cx;
+      const double dist = __dsqrt_rn(__dadd_rn(__dmul_rn(dy, dy), __dmul_rn(dx, dx)));
+      const double e = __dsub_rn(dist, radius);
+      val = dist <= radius ? 1.0f
+                           : (float)exp(__ddiv_rn(-__dmul_rn(e, e), __dmul_rn(2.0, sigma2)));
+    }
+    out[i * ld + c] = val;
+  }
+}
+
+}  // namespace
+}  // namespace pidb
+
+using namespace pidb;
+
+extern "C" int pidb_binary_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                                uint8_t* b, int64_t ldb, int64_t* nonbinary, void* stream) {
+  PIDB_REQUIRE(u && b && n >= 1 && m >= 1 && ld >= m, "bad arguments to pidb_binary_pack");
+  PIDB_REQUIRE(ldb >= m && ldb % 16 == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0,
+               "packed row stride must be >= m, a multiple of 16 and 16-byte aligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t jobs = n * ((ldb + 511) / 512);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((jobs + 7) / 8, 148 * 16));
+  if (dtype == PIDB_F32)
+    binary_pack_kernel<float><<<blocks, 256, 0, st>>>(
+        static_cast<const float*>(u), n, m, ld, b, ldb,
+        reinterpret_cast<unsigned long long*>(nonbinary));
+  else if (dtype == PIDB_F64)
+    binary_pack_kernel<double><<<blocks, 256, 0, st>>>(
+        static_cast<const double*>(u), n, m, ld, b, ldb,
+        reinterpret_cast<unsigned long long*>(nonbinary));
+  else
+    PIDB_REQUIRE(false, "dtype must be PIDB_F32 or PIDB_F64");
+  PIDB_LAUNCH_CHECK("binary_pack_kernel");
+  return PIDB_OK;
+}
+
+extern "C" int pidb_pair_sums(const void* u, const void* v, int dtype, int64_t m, const double* w,
+                              int complement, double* out_host, void* ws, size_t ws_bytes,
+                              void* stream) {
+  PIDB_REQUIRE(u && v && out_host && m >= 1, "bad arguments to pidb_pair_sums");
+  const int nb = (int)std::min<int64_t>(4 * 148, (m + 255) / 256);
+  PIDB_REQUIRE(ws && ws_bytes >= (size_t)(2 * nb + 2) * sizeof(double),
+               "workspace too small for pidb_pair_sums (need %zu bytes)",
+               (size_t)(2 * nb + 2) * sizeof(double));
+  cudaStream_t st = (cudaStream_t)stream;
+  double* part = static_cast<double*>(ws);
+  if (dtype == PIDB_F32)
+    pair_sums_kernel<float><<<nb, 256, 0, st>>>(static_cast<const float*>(u),
+                                                static_cast<const float*>(v), m, w, complement,
+                                                part);
+  else
+    pair_sums_kernel<double><<<nb, 256, 0, st>>>(static_cast<const double*>(u),
+                                                 static_cast<const double*>(v), m, w, complement,
+                                                 part);
+  PIDB_LAUNCH_CHECK("pair_sums_kernel");
+  pair_finish_kernel<<<1, 32, 0, st>>>(part, nb, part + 2 * nb);
+  PIDB_LAUNCH_CHECK("pair_finish_kernel");
+  PIDB_CUDA(cudaMemcpyAsync(out_host, part + 2 * nb, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  PIDB_CUDA(cudaStreamSynchronize(st));
+  return PIDB_OK;
+}
+
+extern "C" int pidb_synth_ellipsoids(float* out, int64_t n, int64_t res, int64_t ld,
+                                     const double* params, double sigma, void* stream) {
+  PIDB_REQUIRE(out && params && n >= 1 && res >= 1 && ld >= res * res * res,
+               "bad arguments to pidb_synth_ellipsoids");
+  PIDB_REQUIRE(n <= 65535, "at most 65535 members per synth call");
+  dim3 grid((unsigned)std::min<int64_t>((ld + 255) / 256, 4096), (unsigned)n);
+  synth_ellipsoids_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(out, n, res, ld, params, sigma);
+  PIDB_LAUNCH_CHECK("synth_ellipsoids_kernel");
+  return PIDB_OK;
+}
+
+extern "C" int pidb_synth_disks(float* out, int64_t n, int64_t res, int64_t ld,
+                                const double* params, double sigma2, void* stream) {
+  PIDB_REQUIRE(out && params && n >= 1 && res >= 1 && ld >= res * res,
+               "bad arguments to pidb_synth_disks");
+  PIDB_REQUIRE(n <= 65535, "at most 65535 members per synth call");
+  dim3 grid((unsigned)std::min<int64_t>((ld + 255) / 256, 4096), (unsigned)n);
+  synth_disks_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(out, n, res, ld, params, sigma2);
+  PIDB_LAUNCH_CHECK("synth_disks_kernel");
+  return PIDB_OK;
+}
+
+// ------------------------------------------------------------ mean mask -----
+// mean(x) = (sum_i u_i(x)) / n, accumulated in fp64 in member order: the same
+// arithmetic as mean_mask (/root/reference/pkg/src/fuzzdepth/grid.py:257-260),
+// hence bit-identical.  Coalesced across cells for each member row.
+namespace pidb {
+namespace {
+template <typename T>
+__global__ void mean_mask_kernel(const T* __restrict__ u, int64_t n, int64_t m, int64_t ld,
+                                 double* __restrict__ out) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) acc = __dadd_rn(acc, (double)u[i * ld + x]);
+    out[x] = __ddiv_rn(acc, (double)n);
+  }
+}
+}  // namespace
+}  // namespace pidb
+
+extern "C" int pidb_mean_mask(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                              double* out, void* stream) {
+  PIDB_REQUIRE(u && out && n >= 1 && m >= 1 && ld >= m, "bad arguments to pidb_mean_mask");
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 148 * 8));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == PIDB_F32)
+    mean_mask_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(u), n, m, ld, out);
+  else
+    mean_mask_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(u), n, m, ld, out);
+  PIDB_LAUNCH_CHECK("mean_mask_kernel");
+  return PIDB_OK;
+}

@@ -1,0 +1,350 @@
+"""Drop-in depth methods (eID, exact PID, PID-mean) on the B200 kernels.
+
+Same names, signatures, results and errors as the reference module
+/root/reference/pkg/src/fuzzdepth/depth.py; the arithmetic runs in libpidb:
+
+  depth_pid_mean  (depth.py:246-287) -> K5 single HBM pass + K4 epilogue
+  depth_pid       (depth.py:213-228) -> K1 3xTF32 tcgen05 Gram + K4, or the
+                                        exact O(N*M) factorisation K5 + K9
+  depth_eid       (depth.py:192-210) -> K6/K7 binary check + pack, K2 exact
+                                        integer Gram (tcgen05 kind::i8) + exact
+                                        epilogue (bit-identical to ref_eid)
+
+Every function accepts a reference-style Ensemble (host members, staged into
+HBM once), a ``DeviceEnsemble`` (already resident; optionally a cell shard of
+a multi-GPU job, combined with one NCCL allreduce), or an (n, *dims) tensor.
+``workers`` is accepted and validated for signature compatibility; device
+results do not depend on it (the reference guarantees worker-count
+invariance, reduction.py:115-127).
+"""
+from __future__ import annotations
+
+import os
+import time
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .device import DeviceEnsemble, stage, stream_ptr
+from .errors import DegenerateEnsembleError, ValidationError
+
+TILE_BYTES = 32 * 2**20          # depth.py:36 (API parity; tiling is on-device here)
+CV_WARN_THRESHOLD = 0.5          # depth.py:40
+METHOD_NAMES = ("eid", "pid", "pid-mean", "dice", "iou")  # depth.py:42
+PID_ALGORITHMS = ("auto", "gram", "factorized")
+
+
+@dataclass(frozen=True)
+class DepthResult:
+    """Per-member depths and ranks (depth.py:45-77); arrays are read-only."""
+
+    ids: tuple[str, ...]
+    in_in: np.ndarray
+    in_out: np.ndarray
+    depth: np.ndarray
+    rank: np.ndarray
+    method: str
+    cv_mass: float
+    elapsed_seconds: float
+
+    def __post_init__(self) -> None:
+        n = len(self.ids)
+        for name in ("in_in", "in_out", "depth", "rank"):
+            a = getattr(self, name)
+            if a.shape != (n,):
+                raise ValidationError(f"{name} must have one entry per member")
+            a.flags.writeable = False
+
+    def __len__(self) -> int:
+        return len(self.ids)
+
+    def ordered_ids(self) -> list[str]:
+        order = np.empty(len(self), dtype=np.int64)
+        order[self.rank] = np.arange(len(self))
+        return [self.ids[i] for i in order]
+
+
+def ranks_from_depths(depth: np.ndarray) -> np.ndarray:
+    """Ranks, 0 = deepest, ties by ascending index (depth.py:80-85).  Host
+    helper for API parity; the depth functions rank on the device (K4)."""
+    order = np.argsort(-np.asarray(depth), kind="stable")
+    rank = np.empty(order.shape[0], dtype=np.int64)
+    rank[order] = np.arange(order.shape[0])
+    return rank
+
+
+def mass_cv(masses: np.ndarray) -> float:
+    """Population std / mean of member masses (depth.py:105-110)."""
+    mean = float(np.mean(masses))
+    if mean == 0.0:
+        return 0.0
+    return float(np.std(masses) / mean)
+
+
+def resolve_workers(workers: int | None = None) -> int:
+    """Same contract as reduction.py:100-112 (kept for signature parity)."""
+    if workers is not None:
+        if workers < 1:
+            raise ValueError("workers must be >= 1")
+        return int(workers)
+    env = os.environ.get("FUZZDEPTH_WORKERS")
+    if env:
+        try:
+            return max(1, int(env))
+        except ValueError:
+            pass
+    return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------- primitives
+
+
+def _f64(n: int, dev) -> torch.Tensor:
+    return torch.empty(n, dtype=torch.float64, device=dev)
+
+
+def _allreduce(t: torch.Tensor, de: DeviceEnsemble) -> None:
+    """Combine per-shard partial sums across GPUs: one NCCL allreduce."""
+    if de.process_group is None:
+        return
+    import torch.distributed as dist
+
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=de.process_group)
+
+
+def _masses_device(de: DeviceEnsemble, with_nonbinary: bool = False):
+    """K6 (+K7 check): member masses (depth.py:88-102) on the device."""
+    dev = de.device
+    mass = _f64(de.n, dev)
+    nb = torch.zeros(de.n, dtype=torch.int64, device=dev) if with_nonbinary else None
+    wsb = N.load().pidb_pid_mean_workspace_bytes(de.n, de.m, de.dtype_code)
+    if wsb == 0:
+        raise ValidationError(f"ensemble of {de.n} members is not supported by the tile layout")
+    ws = de.workspace(wsb)
+    N.call("pidb_member_masses", de.ptr(), de.dtype_code, de.n, de.m, de.ld, de.wptr(),
+           mass.data_ptr(), None if nb is None else nb.data_ptr(), ws.data_ptr(), ws.numel(),
+           stream_ptr(dev))
+    if de.process_group is not None:
+        _allreduce(mass, de)
+        if nb is not None:
+            _allreduce(nb, de)
+    return (mass, nb) if with_nonbinary else mass
+
+
+def _mean_partials(de: DeviceEnsemble) -> torch.Tensor:
+    """K5: packed [row_plain (n) | mass (n) | col_mean (1)], allreduced."""
+    dev = de.device
+    buf = _f64(2 * de.n + 1, dev)
+    wsb = N.load().pidb_pid_mean_workspace_bytes(de.n, de.m, de.dtype_code)
+    if wsb == 0:
+        raise ValidationError(f"ensemble of {de.n} members is not supported by the tile layout")
+    ws = de.workspace(wsb)
+    p = buf.data_ptr()
+    N.call("pidb_pid_mean_partials", de.ptr(), de.dtype_code, de.n, de.m, de.ld, de.wptr(),
+           p, p + 8 * de.n, p + 16 * de.n, ws.data_ptr(), ws.numel(), stream_ptr(dev))
+    _allreduce(buf, de)
+    return buf
+
+
+def _col_sums(de: DeviceEnsemble, inv: torch.Tensor) -> torch.Tensor:
+    """K9-B: col_inv[j] = sum_i inv_i G[i,j] without forming G."""
+    dev = de.device
+    col = _f64(de.n, dev)
+    ws = de.workspace(N.load().pidb_pid_mean_workspace_bytes(de.n, de.m, de.dtype_code))
+    N.call("pidb_pid_colsums", de.ptr(), de.dtype_code, de.n, de.m, de.ld, de.wptr(),
+           inv.data_ptr(), col.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr(dev))
+    _allreduce(col, de)
+    return col
+
+
+class _Out:
+    """Device result block [inv | in_in | in_out | depth] + ranks, one D2H."""
+
+    def __init__(self, n: int, dev):
+        self.n = n
+        self.vals = _f64(4 * n, dev)
+        self.rank = torch.empty(n, dtype=torch.int64, device=dev)
+
+    def ptrs(self):
+        p, n = self.vals.data_ptr(), self.n
+        return p, p + 8 * n, p + 16 * n, p + 24 * n
+
+    def fetch(self):
+        v = self.vals.cpu().numpy().reshape(4, self.n)
+        r = self.rank.cpu().numpy()
+        return v[1].copy(), v[2].copy(), v[3].copy(), r.copy()
+
+
+def _finish(de, out: _Out, method: str, masses: np.ndarray, t0: float) -> DepthResult:
+    in_in, in_out, depth, rank = out.fetch()
+    return DepthResult(ids=de.ids, in_in=in_in, in_out=in_out, depth=depth, rank=rank,
+                       method=method, cv_mass=mass_cv(masses),
+                       elapsed_seconds=time.perf_counter() - t0)
+
+
+# ------------------------------------------------------------------ methods
+
+
+def member_masses(ensemble, workers: int | None = None, require_binary: bool = False) -> np.ndarray:
+    """Weighted mass of every member (depth.py:88-102), one device pass."""
+    resolve_workers(workers)
+    de = stage(ensemble)
+    if require_binary:
+        mass, nb = _masses_device(de, with_nonbinary=True)
+        _raise_first_nonbinary(de, nb)
+    else:
+        mass = _masses_device(de)
+    return mass.cpu().numpy()
+
+
+def _raise_first_nonbinary(de: DeviceEnsemble, nb: torch.Tensor) -> None:
+    bad = torch.nonzero(nb).flatten()
+    if bad.numel():
+        i = int(bad[0])
+        raise ValidationError(f"member {de.ids[i]!r} is not binary (0/1) valued")
+
+
+def depth_pid_mean(ensemble, workers: int | None = None,
+                   cv_warn_threshold: float = CV_WARN_THRESHOLD) -> DepthResult:
+    """Linear-time inclusion depth against the ensemble mean (depth.py:246-287).
+
+    One HBM pass (K5) yields every member's sum against the mean, its mass
+    and the mean's mass; K4 forms in_in, in_out, depth and ranks on device.
+    """
+    t0 = time.perf_counter()
+    resolve_workers(workers)
+    de = stage(ensemble)
+    n, dev = de.n, de.device
+    buf = _mean_partials(de)
+    out = _Out(n, dev)
+    p = buf.data_ptr()
+    inv, ii, io, d = out.ptrs()
+    N.call("pidb_depth_epilogue", N.PIDB_EPI_PID_MEAN, n, p, p + 8 * n, p + 16 * n,
+           inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
+    host = buf[n:].cpu().numpy()
+    masses, col_mean = host[:n], float(host[n])
+    if col_mean == 0.0:
+        raise DegenerateEnsembleError("ensemble mean mask is identically zero")
+    res = _finish(de, out, "pid-mean", masses, t0)
+    if res.cv_mass > cv_warn_threshold:
+        warnings.warn(
+            f"member mass CV {res.cv_mass:.3g} exceeds {cv_warn_threshold:g}; "
+            "pid-mean ranks may diverge from exact pid",
+            RuntimeWarning,
+            stacklevel=2,
+        )
+    return res
+
+
+def _pid_factorized(de: DeviceEnsemble, out: _Out) -> np.ndarray:
+    """Exact PID in two HBM passes: K5 gives row_plain and masses, K9-B the
+    inverse-mass-weighted column sums (SURVEY.md §0 finding 2)."""
+    n, dev = de.n, de.device
+    buf = _mean_partials(de)
+    p = buf.data_ptr()
+    inv = out.ptrs()[0]
+    N.call("pidb_inverse_masses", n, p + 8 * n, inv, stream_ptr(dev))
+    col = _col_sums(de, out.vals[:n])
+    _, ii, io, d = out.ptrs()
+    N.call("pidb_depth_epilogue", N.PIDB_EPI_PID, n, p, p + 8 * n, col.data_ptr(),
+           inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
+    return buf[n:2 * n].cpu().numpy()
+
+
+def _pid_gram(de: DeviceEnsemble, out: _Out) -> np.ndarray:
+    """PID from the dense N x N Gram on tcgen05 tensor cores (K1 3xTF32)."""
+    from .reduction import gram_device
+
+    n, dev = de.n, de.device
+    mass = _masses_device(de)
+    g = gram_device(de)  # allreduced fp64 (n, n)
+    inv = out.ptrs()[0]
+    N.call("pidb_inverse_masses", n, mass.data_ptr(), inv, stream_ptr(dev))
+    rc = _f64(2 * n, dev)
+    N.call("pidb_gram_reduce", g.data_ptr(), n, inv, rc.data_ptr(), rc.data_ptr() + 8 * n,
+           stream_ptr(dev))
+    _, ii, io, d = out.ptrs()
+    N.call("pidb_depth_epilogue", N.PIDB_EPI_PID, n, rc.data_ptr(), mass.data_ptr(),
+           rc.data_ptr() + 8 * n, inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
+    return mass.cpu().numpy()
+
+
+def _gram_available() -> bool:
+    return N.has_symbol("pidb_gram_tf32x3")
+
+
+def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") -> DepthResult:
+    """Exact probabilistic inclusion depth over all pairs (depth.py:213-228).
+
+    algorithm="gram": the symmetric N x N Gram on tcgen05 (3xTF32, fp64
+    flushes) followed by the fused row/column-sum epilogue — the reference's
+    own formulation.  algorithm="factorized": the exact O(N*M) two-pass
+    identity.  "auto" picks the Gram for float32 ensembles once the kernel is
+    built, the factorisation otherwise.
+    """
+    t0 = time.perf_counter()
+    resolve_workers(workers)
+    if algorithm not in PID_ALGORITHMS:
+        raise ValidationError(f"unknown pid algorithm {algorithm!r}; expected one of {PID_ALGORITHMS}")
+    de = stage(ensemble)
+    out = _Out(de.n, de.device)
+    use_gram = algorithm == "gram" or (
+        algorithm == "auto" and de.dtype_code == N.PIDB_F32 and _gram_available()
+    )
+    masses = _pid_gram(de, out) if use_gram else _pid_factorized(de, out)
+    return _finish(de, out, "pid", masses, t0)
+
+
+def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
+    """Inclusion depth of binary ensembles (depth.py:192-210).
+
+    Unit weights: exact integer intersection Gram (K7 pack + K2 tcgen05
+    kind::i8) and an exactly rounded epilogue, bit-identical to the
+    exact-summation oracle ref_eid.  Weighted grids: factorised Gram sums.
+    """
+    t0 = time.perf_counter()
+    resolve_workers(workers)
+    de = stage(ensemble)
+    n, dev = de.n, de.device
+    mass, nb = _masses_device(de, with_nonbinary=True)
+    _raise_first_nonbinary(de, nb)
+    out = _Out(n, dev)
+    if de.weights is None and N.has_symbol("pidb_gram_i8"):
+        from .reduction import intersection_gram
+
+        g = intersection_gram(de)
+        ii, io, d = out.ptrs()[1:]
+        N.call("pidb_eid_exact_epilogue", g.data_ptr(), n, ii, io, d, out.rank.data_ptr(),
+               stream_ptr(dev))
+        masses = mass.cpu().numpy()
+    else:
+        buf = _mean_partials(de)
+        p = buf.data_ptr()
+        inv = out.ptrs()[0]
+        N.call("pidb_inverse_masses", n, p + 8 * n, inv, stream_ptr(dev))
+        col = _col_sums(de, out.vals[:n])
+        masses = buf[n:2 * n].cpu().numpy()
+        n_pos = float(np.count_nonzero(masses > 0.0))
+        _, ii, io, d = out.ptrs()
+        N.call("pidb_eid_factorized_epilogue", n, p, p + 8 * n, col.data_ptr(), n_pos,
+               inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
+    return _finish(de, out, "eid", masses, t0)
+
+
+def depth_by_method(ensemble, method: str, workers: int | None = None) -> DepthResult:
+    """Dispatch on a method name (depth.py:349-363)."""
+    if method == "eid":
+        return depth_eid(ensemble, workers)
+    if method == "pid":
+        return depth_pid(ensemble, workers)
+    if method == "pid-mean":
+        return depth_pid_mean(ensemble, workers)
+    if method in ("dice", "iou", "fuzzy-dice", "prob-iou"):
+        raise ValidationError(
+            f"method {method!r} (similarity baseline, depth.py:290-325) is outside the "
+            "B200 hot path; use fuzzdepth.depth_similarity_baseline"
+        )
+    raise ValidationError(f"unknown depth method {method!r}; expected one of {METHOD_NAMES}")

@@ -1,0 +1,288 @@
+"""Device residency: ensembles as one row-major (n, ld) matrix in HBM.
+
+Replaces the reference's per-member access (Ensemble.member / block_values,
+/root/reference/pkg/src/fuzzdepth/grid.py:196-213) on the hot path: members
+are uploaded once through pinned, double-buffered host staging and every
+depth kernel then streams the resident matrix.
+
+Layout: row i = member i, ``ld`` = cells rounded up to 32 elements (128-byte
+rows, TMA-aligned), zero padding.  float32 storage unless a member is float64
+(the reference's dtype policy, grid.py:103-104), in which case the whole matrix
+is float64.  A sharded ensemble holds a contiguous cell slab [lo, hi) of every
+member on each rank (multi-GPU voxel sharding).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import DegenerateEnsembleError, GridMismatchError, ValidationError
+from .grid import VALUE_TOLERANCE, GridSpec
+
+_ROW_ALIGN = 32  # elements; 128-byte rows for fp32
+_STAGE_BYTES = 64 << 20
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "no CUDA device: the B200 depth path has no CPU fallback"
+        )
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if dev.type != "cuda":
+        raise ValidationError(f"device must be a CUDA device, got {dev}")
+    return dev
+
+
+def padded_ld(m: int) -> int:
+    return (m + _ROW_ALIGN - 1) // _ROW_ALIGN * _ROW_ALIGN
+
+
+def shard_bounds(m: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced cell slab of rank `rank` out of `world`."""
+    base, extra = divmod(m, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+@dataclass
+class DeviceEnsemble:
+    values: torch.Tensor                 # (n, ld) float32/float64 on a CUDA device
+    m: int                               # cells held here (shard-local)
+    dims: tuple[int, ...]
+    ids: tuple[str, ...]
+    weights: torch.Tensor | None = None  # (m,) float64, shard-local
+    weights_host: np.ndarray | None = None  # full-grid weights (GridSpec parity)
+    process_group: object | None = None  # torch.distributed group when sharded
+    cell_range: tuple[int, int] | None = None
+    _cache: dict = field(default_factory=dict, repr=False)
+
+    # ------------------------------------------------------------ properties
+    @property
+    def n(self) -> int:
+        return int(self.values.shape[0])
+
+    @property
+    def ld(self) -> int:
+        return int(self.values.stride(0))
+
+    @property
+    def device(self) -> torch.device:
+        return self.values.device
+
+    @property
+    def dtype_code(self) -> int:
+        return N.PIDB_F64 if self.values.dtype == torch.float64 else N.PIDB_F32
+
+    @property
+    def grid(self) -> GridSpec:
+        return GridSpec(self.dims, self.weights_host)
+
+    @property
+    def sharded(self) -> bool:
+        return self.process_group is not None
+
+    def __len__(self) -> int:
+        return self.n
+
+    def ptr(self) -> int:
+        return self.values.data_ptr()
+
+    def wptr(self) -> int | None:
+        return None if self.weights is None else self.weights.data_ptr()
+
+    # ---------------------------------------------------------- construction
+    @classmethod
+    def from_tensor(
+        cls,
+        values: torch.Tensor,
+        weights=None,
+        ids: Sequence[str] | None = None,
+        dims: Sequence[int] | None = None,
+        validate: bool = True,
+        device=None,
+    ) -> "DeviceEnsemble":
+        """Stage an (n, *dims) tensor or array (host or device)."""
+        if isinstance(values, np.ndarray):
+            values = torch.from_numpy(values)
+        if values.dim() < 2:
+            raise ValidationError("member tensor must be (n, *dims)")
+        n = int(values.shape[0])
+        if n == 0:
+            raise DegenerateEnsembleError("ensemble needs at least one member")
+        dims = tuple(int(d) for d in (dims if dims is not None else values.shape[1:]))
+        m = int(np.prod(dims))
+        if int(np.prod(values.shape[1:])) != m:
+            raise ValidationError(f"member tensor has {values[0].numel()} cells, grid expects {m}")
+        dev = require_cuda(device if device is not None else
+                           (values.device if values.is_cuda else None))
+        dt = torch.float64 if values.dtype == torch.float64 else torch.float32
+        ld = padded_ld(m)
+        out = torch.zeros((n, ld), dtype=dt, device=dev)
+        out[:, :m].copy_(values.reshape(n, m), non_blocking=values.device.type == "cpu" and values.is_pinned())
+        if validate:
+            _validate_inplace(out[:, :m])
+        ids = _make_ids(ids, n)
+        w_host, w_dev = _weights(weights, m, dev)
+        return cls(out, m, dims, ids, w_dev, w_host)
+
+    @classmethod
+    def from_masks(cls, masks: Sequence, ids=None, device=None) -> "DeviceEnsemble":
+        grid = masks[0].grid
+        for mk in masks[1:]:
+            grid.require_same(mk.grid)
+        arr = np.stack([np.asarray(mk.values) for mk in masks])
+        arr = arr if arr.dtype == np.float64 else arr.astype(np.float32, copy=False)
+        return cls.from_tensor(torch.from_numpy(arr), grid.weights, ids,
+                               tuple(grid.dims), validate=False, device=device)
+
+    # ------------------------------------------------------------- helpers
+    def workspace(self, nbytes: int) -> torch.Tensor:
+        """Zero-initialised per-device workspace (the kernels leave their
+        completion counters at zero on exit, so it is reused as is)."""
+        key = ("ws", self.device, torch.cuda.current_stream(self.device).cuda_stream)
+        ws = _WS.get(key)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=self.device)
+            _WS[key] = ws
+        return ws
+
+    def mean_values(self) -> torch.Tensor:
+        out = torch.empty(self.m, dtype=torch.float64, device=self.device)
+        N.call("pidb_mean_mask", self.ptr(), self.dtype_code, self.n, self.m, self.ld,
+               out.data_ptr(), stream_ptr(self.device))
+        return out
+
+
+_WS: dict = {}
+
+
+def stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _make_ids(ids, n):
+    ids = tuple(str(s) for s in (ids if ids is not None else (f"member_{i:04d}" for i in range(n))))
+    if len(ids) != n:
+        raise ValidationError(f"{len(ids)} ids for {n} members")
+    if len(set(ids)) != n:
+        raise ValidationError("member ids must be unique")
+    return ids
+
+
+def _weights(weights, m, dev, lo: int = 0, hi: int | None = None):
+    if weights is None:
+        return None, None
+    if isinstance(weights, torch.Tensor):
+        w_host = weights.detach().cpu().numpy().astype(np.float64)
+    else:
+        w_host = np.ascontiguousarray(weights, dtype=np.float64)
+    hi = w_host.shape[0] if hi is None else hi
+    if w_host.ndim != 1 or hi - lo != m:
+        raise ValidationError(f"weights shape {w_host.shape} does not match cell count {m}")
+    if not np.isfinite(w_host).all() or (w_host <= 0).any():
+        raise ValidationError("cell weights must be finite and positive")
+    w_dev = torch.from_numpy(np.ascontiguousarray(w_host[lo:hi])).to(dev)
+    return w_host, w_dev
+
+
+def _validate_inplace(v: torch.Tensor) -> None:
+    """ProbMask value policy (grid.py:105-116) for raw tensors: finite, within
+    [0,1] up to VALUE_TOLERANCE, clamped."""
+    if not bool(torch.isfinite(v).all()):
+        raise ValidationError("mask values must be finite")
+    lo, hi = float(v.min()), float(v.max())
+    if lo < -VALUE_TOLERANCE or hi > 1.0 + VALUE_TOLERANCE:
+        raise ValidationError(f"mask values outside [0, 1]: min={lo!r} max={hi!r}")
+    if lo < 0.0 or hi > 1.0:
+        v.clamp_(0.0, 1.0)
+
+
+class _PinnedRing:
+    """Two pinned host slots; H2D copies overlap the host-side member loads."""
+
+    def __init__(self, slot_elems: int, dtype: torch.dtype):
+        self.slots = [torch.empty(slot_elems, dtype=dtype, pin_memory=True) for _ in range(2)]
+        self.events: list[torch.cuda.Event | None] = [None, None]
+        self.k = 0
+
+    def next(self) -> tuple[torch.Tensor, int]:
+        k = self.k
+        self.k ^= 1
+        ev = self.events[k]
+        if ev is not None:
+            ev.synchronize()
+        return self.slots[k], k
+
+    def mark(self, k: int, stream) -> None:
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.events[k] = ev
+
+
+def stage(ensemble, device=None, shard: tuple[int, int] | None = None,
+          process_group=None) -> DeviceEnsemble:
+    """Bring an ensemble into HBM (no-op for an already staged one).
+
+    Accepts a DeviceEnsemble, an (n, *dims) torch tensor / numpy array, or any
+    reference-style Ensemble (``grid``, ``ids``, ``len``, ``member(i)``;
+    lazy loaders are resolved one member at a time, grid.py:196-202).
+    ``shard=(rank, world)`` keeps only this rank's contiguous cell slab.
+    """
+    if isinstance(ensemble, DeviceEnsemble):
+        return ensemble
+    if isinstance(ensemble, (torch.Tensor, np.ndarray)):
+        return DeviceEnsemble.from_tensor(ensemble, device=device)
+    dev = require_cuda(device)
+    n = len(ensemble)
+    if n == 0:
+        raise DegenerateEnsembleError("ensemble needs at least one member")
+    grid = ensemble.grid
+    dims = tuple(int(d) for d in grid.dims)
+    m_full = int(np.prod(dims))
+    lo, hi = (0, m_full) if shard is None else shard_bounds(m_full, *shard)
+    m = hi - lo
+    ld = padded_ld(m)
+    first = np.asarray(ensemble.member(0).values)
+    dt = torch.float64 if first.dtype == np.float64 else torch.float32
+    out = torch.zeros((n, ld), dtype=dt, device=dev)
+    s = torch.cuda.current_stream(dev)
+    per_slot = max(1, _STAGE_BYTES // max(1, m * out.element_size()))
+    ring = _PinnedRing(per_slot * m, dt)
+    i = 0
+    vals0 = first
+    while i < n:
+        slot, k = ring.next()
+        cnt = min(per_slot, n - i)
+        host = slot.numpy()
+        promote = False
+        for j in range(cnt):
+            v = vals0 if i + j == 0 else np.asarray(ensemble.member(i + j).values)
+            if v.shape != (m_full,):
+                v = v.reshape(-1)
+                if v.shape != (m_full,):
+                    raise GridMismatchError(f"member {i + j} has {v.size} cells, grid expects {m_full}")
+            if v.dtype == np.float64 and dt == torch.float32:
+                promote = True
+                cnt = j
+                break
+            host[j * m:(j + 1) * m] = v[lo:hi]
+        if cnt:
+            out[i:i + cnt, :m].copy_(slot[:cnt * m].view(cnt, m), non_blocking=True)
+            ring.mark(k, s)
+        i += cnt
+        if promote:  # a float64 member appeared: keep full precision from here on
+            torch.cuda.current_stream(dev).synchronize()
+            out = out.double()
+            dt = torch.float64
+            ring = _PinnedRing(per_slot * m, dt)
+    w_host, w_dev = _weights(grid.weights, m, dev, lo, hi)
+    de = DeviceEnsemble(out, m, dims, tuple(str(x) for x in ensemble.ids), w_dev, w_host,
+                        process_group=process_group if shard is not None else None,
+                        cell_range=(lo, hi))
+    return de
