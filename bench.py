@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 depth hot path (contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[4], the largest single-GPU PID-mean config):
+PID-mean on a 200-member 512^3 fp32 fuzzy-ellipsoid ensemble (107.4 GB), the
+reference generator's recipe evaluated on the device.  A "step" is one full
+depth_pid_mean call (K5 single HBM pass + allreduce when N>1 + K4 epilogue +
+result D2H).  ``value`` = member-voxels/s with the ensemble resident in HBM;
+``e2e`` = the same call on a pinned HOST tensor (H2D staging, validation,
+kernels and result D2H inside the timed region).  The secondary ``pid``
+object reports exact PID on BASELINE configs[3] (1000 x 256^3).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (voxel-sharded, NCCL)
+
+``--impl reference`` times the reference algorithm's CPU restatement
+(oracle.port, numpy/OpenBLAS, all host threads) on a bounded sample of the
+same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (method, res, members, description)
+    "cfg1": ("pid-mean", 256, 100, "cfg1: 2D fuzzy disks, 100 members 256^2"),
+    "cfg3": ("pid-mean", 128, 200, "cfg3: PID-mean, 200 fuzzy ellipsoids 128^3 fp32"),
+    "cfg4": ("pid", 256, 1000, "cfg4: PID, 1000 fuzzy ellipsoids 256^3 fp32"),
+    "cfg5": ("pid-mean", 512, 200, "cfg5: PID-mean, 200 fuzzy ellipsoids 512^3 fp32 (107.4 GB)"),
+}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "src": "measured (MEASURED_PEAKS.json)",
+                "bf16": d.get("bf16_tflops", 1590.0)}
+    return {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)", "bf16": 1590.0}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ helpers
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist.group.WORLD
+    return rank, world, local, pg
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def timed(step, steps, warmup, world, sampler=None):
+    """W untimed steps, then K steps between barrier+sync, device events."""
+    import torch
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    if sampler:
+        sampler.__enter__()
+        time.sleep(0.3)
+    a.record()
+    for _ in range(steps):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__()
+    barrier(world)
+    ms = a.elapsed_time(b) / steps
+    return max_over_ranks(ms, world)
+
+
+def kernel_ms(events, name):
+    ts = [a.elapsed_time(b) for nm, a, b in events if nm == name]
+    return (float(np.mean(ts)) if ts else None), len(ts)
+
+
+def ellipsoid_sample_cpu(res, n, y_planes, seed=0):
+    """Bounded CPU sample of the cfg ellipsoid workload: all n members on
+    `y_planes` central planes (generated with torch on the host cores)."""
+    import torch
+
+    from paper_2512_15187_b200.synth import ellipsoid_params
+
+    prm, sigma, _ = ellipsoid_params(res, n, 0, seed)
+    y0 = res // 2 - y_planes // 2
+    y = torch.arange(y0, y0 + y_planes, dtype=torch.float64).view(-1, 1, 1)
+    x = torch.arange(res, dtype=torch.float64).view(1, -1, 1)
+    z = torch.arange(res, dtype=torch.float64).view(1, 1, -1)
+    out = np.empty((n, y_planes * res * res), dtype=np.float32)
+    for i in range(n):
+        cy, cx, cz, ay, ax, az = prm[i]
+        dy, dx, dz = y - cy, x - cx, z - cz
+        rho = torch.sqrt((dy / ay) ** 2 + (dx / ax) ** 2 + (dz / az) ** 2)
+        r = torch.sqrt(dy ** 2 + dx ** 2 + dz ** 2)
+        d = r * (1.0 - 1.0 / rho)
+        u = torch.where(rho > 1.0, torch.exp(-(d ** 2) / (2.0 * sigma * sigma)), torch.ones_like(rho))
+        out[i] = u.to(torch.float32).reshape(-1).numpy()
+    return out
+
+
+def cpu_reference(U, method, workers):
+    from oracle import port
+
+    t0 = time.perf_counter()
+    if method == "pid-mean":
+        port.depth_pid_mean(U, None, workers=workers)
+    else:
+        port.depth_pid(U, None, workers=workers)
+    return time.perf_counter() - t0
+
+
+# ------------------------------------------------------------ reference arm
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    method, res, n, desc = WORKLOADS[args.workload]
+    workers = os.cpu_count() or 1
+    planes = args.ref_planes or (8 if res >= 512 else max(1, res // 16))
+    U = ellipsoid_sample_cpu(res, n, planes) if args.workload != "cfg1" else None
+    if U is None:
+        from paper_2512_15187_b200.synth import disk_params
+
+        raise SystemExit("reference arm supports ellipsoid workloads")
+    if method == "pid":
+        U = U[: min(n, args.ref_pid_members)]
+    mv = U.shape[0] * U.shape[1]
+    for _ in range(args.warmup):
+        cpu_reference(U, method, workers)
+    ts = [cpu_reference(U, method, workers) for _ in range(args.steps)]
+    sec = float(np.mean(ts))
+    value = mv / sec
+    sample = (f"{U.shape[0]} members x {planes} central planes of {res}^3 "
+              f"({U.shape[1]} cells/member) of the {args.workload} workload; oracle.port "
+              f"(numpy/OpenBLAS restatement of fuzzdepth {method}), ThreadPool({workers})")
+    line = {
+        "impl": "reference", "metric": metric_name(method), "value": value,
+        "unit": "member-voxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "member-voxels/s", "cores": workers,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "member-voxels/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def metric_name(method):
+    return "member-voxels/sec for PID-mean" if method == "pid-mean" else "member-voxels/sec for PID"
+
+
+# ------------------------------------------------------------------ our arm
+
+
+def run_ours(args, rank, world, local, pg):
+    import torch
+
+    import paper_2512_15187_b200 as pb
+    from paper_2512_15187_b200 import depth as D
+    from paper_2512_15187_b200 import synth
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    method, res, n, desc = WORKLOADS[args.workload]
+    m_full = res ** 3
+    shard = (rank, world) if world > 1 else None
+    fn = pb.depth_pid_mean if method == "pid-mean" else pb.depth_pid
+    pk = peaks()
+
+    de = synth.ellipsoids_device(res, n, 0, 0, device=dev, shard=shard, process_group=pg)
+    torch.cuda.synchronize()
+    m_local = de.m
+
+    def step():
+        return fn(de)
+
+    D.KERNEL_EVENTS = []
+    sampler = ClockSampler(local) if rank == 0 else None
+    fn(de)  # first call outside the event log (plans, workspace)
+    D.KERNEL_EVENTS = []
+    ms = timed(step, args.steps, args.warmup, world, sampler)
+    kname = "pidb_pid_mean_partials"
+    kms, klaunch = kernel_ms(D.KERNEL_EVENTS, kname)
+    launches_per_step = 3 if method == "pid-mean" else 6
+    D.KERNEL_EVENTS = None
+    total_mv = n * m_full
+    value = total_mv / (ms * 1e-3)
+    alg_bytes = n * m_local * 4
+    achieved = alg_bytes / (kms * 1e-3) / 1e9 if kms else None
+
+    res_chk = fn(de)
+    line = {
+        "metric": metric_name(method), "value": value, "unit": "member-voxels/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference gen_ellipsoid_ensemble recipe: per-member Philox "
+                "parameters on the host, voxels evaluated on the device)",
+        "config": {"workload": desc, "members": n, "cells": m_full, "cells_per_gpu": m_local,
+                   "bytes_per_gpu": alg_bytes, "l2": "no flush: inputs (%.1f GB/GPU) >> 126 MB L2"
+                   % (alg_bytes / 1e9),
+                   "parallelism": f"voxel-sharded x{world}, one NCCL allreduce of 2N+1 fp64"
+                   if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "kernel": "stream_pass_kernel (K5, pidb_pid_mean_partials)",
+                     "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"] if achieved else None, "traffic": None,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "kernel_ms": kms, "launches_timed": klaunch, "peak_src": pk["src"]},
+        "gpu_launches": launches_per_step * args.steps,
+        "min_depth_gap": float(np.min(np.diff(np.sort(res_chk.depth)))) if n > 1 else None,
+    }
+    if sampler is not None:
+        line["clocks"] = sampler.summary()
+
+    # ---------------- CPU baseline (rank 0, N=1): oracle.port on a sample
+    if rank == 0 and world == 1 and not args.no_cpu:
+        planes = args.ref_planes or (8 if res >= 512 else max(1, res // 16))
+        y0 = res // 2 - planes // 2
+        lo, hi = y0 * res * res, (y0 + planes) * res * res
+        U = de.values[:, lo:hi].cpu().numpy()
+        if method == "pid":
+            U = U[: args.ref_pid_members]
+        workers = os.cpu_count() or 1
+        sec = cpu_reference(U, method, workers)
+        line["cpu_baseline"] = {
+            "value": U.shape[0] * U.shape[1] / sec, "unit": "member-voxels/s", "cores": workers,
+            "kind": "port",
+            "sample": f"{U.shape[0]} members x {planes} central planes ({U.shape[1]} cells) "
+                      f"of the same ensemble; oracle.port {method} (fuzzdepth algorithm, "
+                      f"numpy/OpenBLAS), ThreadPool({workers}); PID-mean is GIL-bound "
+                      "(effectively 1 core) as in the reference",
+        }
+
+    # ---------------- end to end from pinned host memory
+    host = None
+    if not args.no_e2e:
+        host, e2e_meta = prepare_e2e(de, world)
+    meta = (de.n, de.m, de.dims, de.cell_range)
+    del de
+    torch.cuda.empty_cache()
+    if not args.no_e2e:
+        line["e2e"] = run_e2e(args, host, e2e_meta, meta, fn, world, pg, dev) if host is not None \
+            else e2e_meta
+        del host
+
+    # ---------------- secondary: exact PID on cfg4
+    if args.workload == "cfg5" and not args.no_pid:
+        line["pid"] = run_pid_secondary(args, rank, world, pg, dev, pk)
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def prepare_e2e(de, world):
+    """Copy the resident ensemble (this rank's slab) into pinned host memory."""
+    import psutil
+    import torch
+
+    need = de.n * de.m * 4
+    avail = psutil.virtual_memory().available
+    if need * world > 0.8 * avail:
+        return None, {"value": None, "unit": "member-voxels/s",
+                      "skipped": f"needs {need * world / 1e9:.1f} GB pinned host memory, "
+                                 f"{avail / 1e9:.1f} GB available"}
+    host = torch.empty((de.n, de.m), dtype=torch.float32, pin_memory=True)
+    host.copy_(de.values[:, :de.m])
+    torch.cuda.synchronize()
+    return host, None
+
+
+def run_e2e(args, host, _, meta, fn, world, pg, dev):
+    from paper_2512_15187_b200.device import DeviceEnsemble
+
+    n, m, dims, cr = meta
+
+    def step():
+        e = DeviceEnsemble.from_tensor(host, dims=dims, process_group=pg,
+                                       cell_range=cr if world > 1 else None, device=dev)
+        return fn(e)
+
+    ms = timed(step, max(1, min(args.steps, 3)), 1, world)
+    total = n * int(np.prod(dims))
+    return {"value": total / (ms * 1e-3), "unit": "member-voxels/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": n * m * 4, "d2h_bytes_per_step": n * 8 * 4 + n * 8 + 24,
+            "path": "depth_pid_mean(DeviceEnsemble.from_tensor(pinned host tensor)): "
+                    "pitched H2D + device validation + K5 + K4 + result D2H"}
+
+
+def run_pid_secondary(args, rank, world, pg, dev, pk):
+    import torch
+
+    import paper_2512_15187_b200 as pb
+    from paper_2512_15187_b200 import depth as D
+    from paper_2512_15187_b200 import synth
+
+    res, n = 256, 1000
+    shard = (rank, world) if world > 1 else None
+    de = synth.ellipsoids_device(res, n, 0, 0, device=dev, shard=shard, process_group=pg)
+    torch.cuda.synchronize()
+    alg = "gram" if D._gram_available() else "factorized"
+    D.KERNEL_EVENTS = []
+    pb.depth_pid(de, algorithm=alg)
+    D.KERNEL_EVENTS = []
+    ms = timed(lambda: pb.depth_pid(de, algorithm=alg), max(1, min(args.steps, 5)), 2, world)
+    ev = D.KERNEL_EVENTS
+    D.KERNEL_EVENTS = None
+    mv = n * res ** 3
+    out = {"workload": "cfg4: PID, 1000 fuzzy ellipsoids 256^3 fp32 (67.1 GB)",
+           "algorithm": alg, "ms_per_depth": ms, "value": mv / (ms * 1e-3),
+           "unit": "member-voxels/s", "pair_voxels_per_s": n * n * res ** 3 / (ms * 1e-3)}
+    if alg == "factorized":
+        k1, _ = kernel_ms(ev, "pidb_pid_mean_partials")
+        k2, _ = kernel_ms(ev, "pidb_pid_colsums")
+        b = n * de.m * 4
+        out["roofline"] = {"bound": "hbm", "achieved": 2 * b / ((k1 + k2) * 1e-3) / 1e9,
+                           "peak": pk["hbm_gbs"], "unit": "GB/s",
+                           "frac": 2 * b / ((k1 + k2) * 1e-3) / 1e9 / pk["hbm_gbs"],
+                           "kernels_ms": [k1, k2], "algorithmic_bytes": 2 * b}
+    else:
+        kg, _ = kernel_ms(ev, "pidb_gram_tf32x3")
+        flops = n * (n + 1) * de.m
+        out["roofline"] = {"bound": "tensor", "achieved": flops / (kg * 1e-3) / 1e12,
+                           "unit": "TFLOP/s", "kernel_ms": kg, "algorithmic_flops": flops}
+    del de
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-pid", action="store_true")
+    ap.add_argument("--ref-planes", type=int, default=0)
+    ap.add_argument("--ref-pid-members", type=int, default=64)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        run_reference(args, rank, world)
+        return
+    rank, world, local, pg = dist_setup()
+    try:
+        run_ours(args, rank, world, local, pg)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -21,6 +21,10 @@
  *     float64, /root/reference/pkg/src/fuzzdepth/grid.py:103-104);
  *   - weights `w` are per-cell float64 (nullable = uniform unit weights,
  *     /root/reference/pkg/src/fuzzdepth/grid.py:39-57);
+ *   - workspaces (ws, ws_bytes) are caller-owned device buffers that must be
+ *     ZERO-FILLED when first allocated; the first 256 bytes hold a completion
+ *     counter that every kernel leaves at zero on exit, so one workspace can
+ *     be reused by consecutive calls on the same stream;
  *   - return 0 on success, a negative PIDB_E* code otherwise; the message is
  *     available from pidb_last_error() (thread-local).
  */
@@ -163,6 +167,19 @@ int pidb_ranks(int64_t n, const double* depth, int64_t* rank, void* stream);
  * (The depth kernels never materialise it; this serves the mean_mask API.) */
 int pidb_mean_mask(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
                    double* out, void* stream);
+
+/* Pitched row copy host<->device (cudaMemcpy2DAsync, cudaMemcpyDefault):
+ * stages an (n, m) host matrix into the padded (n, ld) device layout. */
+int pidb_copy_rows(void* dst, int64_t dst_pitch_bytes, const void* src,
+                   int64_t src_pitch_bytes, int64_t row_bytes, int64_t rows,
+                   void* stream);
+
+/* One-pass value check of raw member data (ProbMask policy, grid.py:105-116):
+ * stats (device, 3 x 8 bytes) = {#non-finite, min key, max key} where the
+ * keys are order-preserving int64 images of the doubles; clamp != 0 clips
+ * values to [0, 1] in place in the same pass. */
+int pidb_validate(void* u, int dtype, int64_t n, int64_t m, int64_t ld, int clamp,
+                  void* stats, void* stream);
 
 /* ---------------------------------------------------------------- K8 ----
  * prob_inclusion (inclusion.py:22-40): out[0] = sum w u v, out[1] = sum w u.

@@ -61,6 +61,8 @@ SIGNATURES: dict[str, tuple] = {
     "pidb_ranks": (_int, [_i64, _p, _p, _p]),
     "pidb_pair_sums": (_int, [_p, _p, _int, _i64, _p, _int, _p, _p, _sz, _p]),
     "pidb_mean_mask": (_int, [_p, _int, _i64, _i64, _i64, _p, _p]),
+    "pidb_copy_rows": (_int, [_p, _i64, _p, _i64, _i64, _i64, _p]),
+    "pidb_validate": (_int, [_p, _int, _i64, _i64, _i64, _int, _p, _p]),
     "pidb_synth_ellipsoids": (_int, [_p, _i64, _i64, _i64, _p, _dbl, _p]),
     "pidb_synth_disks": (_int, [_p, _i64, _i64, _i64, _p, _dbl, _p]),
 }

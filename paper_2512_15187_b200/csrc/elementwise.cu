@@ -252,3 +252,91 @@ extern "C" int pidb_mean_mask(const void* u, int dtype, int64_t n, int64_t m, in
   PIDB_LAUNCH_CHECK("mean_mask_kernel");
   return PIDB_OK;
 }
+
+// ------------------------------------------------------------ staging -------
+// Pitched host<->device row copies (one cudaMemcpy2DAsync per call) so that
+// (n, m) host matrices land in the padded (n, ld) device layout without a
+// device-side temporary.
+extern "C" int pidb_copy_rows(void* dst, int64_t dst_pitch_bytes, const void* src,
+                              int64_t src_pitch_bytes, int64_t row_bytes, int64_t rows,
+                              void* stream) {
+  PIDB_REQUIRE(dst && src && rows >= 0 && row_bytes >= 0 && dst_pitch_bytes >= row_bytes &&
+                   src_pitch_bytes >= row_bytes,
+               "bad arguments to pidb_copy_rows");
+  if (rows == 0 || row_bytes == 0) return PIDB_OK;
+  PIDB_CUDA(cudaMemcpy2DAsync(dst, (size_t)dst_pitch_bytes, src, (size_t)src_pitch_bytes,
+                              (size_t)row_bytes, (size_t)rows, cudaMemcpyDefault,
+                              (cudaStream_t)stream));
+  return PIDB_OK;
+}
+
+// ------------------------------------------------------------ validation ----
+// ProbMask value policy (/root/reference/pkg/src/fuzzdepth/grid.py:105-116) for
+// raw tensors, one pass: stats[0] = #non-finite, stats[1] = min, stats[2] = max
+// (as ordered int64 keys of the doubles).  clamp != 0 additionally clips to [0,1].
+namespace pidb {
+namespace {
+__device__ __forceinline__ long long dkey(double d) {
+  long long b = __double_as_longlong(d);
+  return b >= 0 ? b : (b ^ 0x7FFFFFFFFFFFFFFFLL);
+}
+template <typename T>
+__global__ void validate_kernel(T* __restrict__ u, int64_t n, int64_t m, int64_t ld, int clamp,
+                                unsigned long long* __restrict__ nonfinite,
+                                long long* __restrict__ kmin, long long* __restrict__ kmax) {
+  unsigned long long bad = 0;
+  double lo = 0.0, hi = 0.0;
+  bool any = false;
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    T v = u[i * ld + x];
+    const double d = (double)v;
+    if (!isfinite(d)) { ++bad; continue; }
+    if (!any) { lo = hi = d; any = true; }
+    lo = fmin(lo, d);
+    hi = fmax(hi, d);
+    if (clamp && (d < 0.0 || d > 1.0)) u[i * ld + x] = d < 0.0 ? T(0) : T(1);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    const double l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const double h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    const int a2 = __shfl_xor_sync(0xffffffffu, (int)any, o);
+    if (a2) {
+      lo = any ? fmin(lo, l2) : l2;
+      hi = any ? fmax(hi, h2) : h2;
+      any = true;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (bad) atomicAdd(nonfinite, bad);
+    if (any) {
+      atomicMin(kmin, dkey(lo));
+      atomicMax(kmax, dkey(hi));
+    }
+  }
+}
+}  // namespace
+}  // namespace pidb
+
+extern "C" int pidb_validate(void* u, int dtype, int64_t n, int64_t m, int64_t ld, int clamp,
+                             void* stats, void* stream) {
+  PIDB_REQUIRE(u && stats && n >= 1 && m >= 1 && ld >= m, "bad arguments to pidb_validate");
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* nf = static_cast<unsigned long long*>(stats);
+  long long* kmin = reinterpret_cast<long long*>(nf + 1);
+  long long* kmax = kmin + 1;
+  const long long init[3] = {0, 0x7FFFFFFFFFFFFFFFLL, (long long)0x8000000000000000ULL};
+  PIDB_CUDA(cudaMemcpyAsync(stats, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  const dim3 blocks((unsigned)std::min<int64_t>((m + 255) / 256, 64),
+                    (unsigned)std::min<int64_t>(n, 1024));
+  if (dtype == PIDB_F32)
+    validate_kernel<float><<<blocks, 256, 0, st>>>(static_cast<float*>(u), n, m, ld, clamp, nf,
+                                                   kmin, kmax);
+  else
+    validate_kernel<double><<<blocks, 256, 0, st>>>(static_cast<double*>(u), n, m, ld, clamp, nf,
+                                                    kmin, kmax);
+  PIDB_LAUNCH_CHECK("validate_kernel");
+  return PIDB_OK;
+}

@@ -411,10 +411,10 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
 
 size_t workspace_bytes(const Plan& pl, int64_t n) {
   const int64_t items = (int64_t)pl.ncb * n;
-  size_t b = align_up((size_t)pl.grid * items * 2 * sizeof(double), 256);
+  size_t b = 256;  // completion counter: fixed offset 0, zero between launches
+  b += align_up((size_t)pl.grid * items * 2 * sizeof(double), 256);
   b += align_up((size_t)pl.grid * sizeof(double), 256);
   b += align_up((size_t)pl.grid * n * sizeof(int64_t), 256);
-  b += 256;  // counter
   return b;
 }
 
@@ -482,6 +482,8 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
   const int64_t items = (int64_t)pl.ncb * n;
   char* base = static_cast<char*>(ws);
   StreamParams sp{};
+  sp.counter = reinterpret_cast<unsigned*>(base);
+  base += 256;
   sp.n = n; sp.m = m; sp.tiles = pl.tiles; sp.nrb = pl.nrb; sp.boxr = pl.boxr;
   sp.stages = pl.stages; sp.stage_bytes = pl.stage_bytes; sp.mode = mode;
   sp.w = w; sp.inv = inv;
@@ -491,7 +493,6 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
   base += align_up((size_t)pl.grid * sizeof(double), 256);
   sp.part_nb = out_nb ? reinterpret_cast<int64_t*>(base) : nullptr;
   base += align_up((size_t)pl.grid * n * sizeof(int64_t), 256);
-  sp.counter = reinterpret_cast<unsigned*>(base);
   sp.out_row = out_row; sp.out_mass = out_mass; sp.out_col = out_col; sp.out_nb = out_nb;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   return dtype == PIDB_F32 ? launch_layout<float>(tm, sp, pl, st)

@@ -101,6 +101,24 @@ def resolve_workers(workers: int | None = None) -> int:
 
 # --------------------------------------------------------------- primitives
 
+# Optional per-kernel CUDA-event log used by bench.py: when a list, every
+# hot-kernel launch appends (name, start_event, end_event) recorded on the
+# launching stream.
+KERNEL_EVENTS: list | None = None
+
+
+def _launch(name: str, *args) -> None:
+    if KERNEL_EVENTS is None:
+        N.call(name, *args)
+        return
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    N.call(name, *args)
+    b.record()
+    KERNEL_EVENTS.append((name, a, b))
+
+
 
 def _f64(n: int, dev) -> torch.Tensor:
     return torch.empty(n, dtype=torch.float64, device=dev)
@@ -124,7 +142,7 @@ def _masses_device(de: DeviceEnsemble, with_nonbinary: bool = False):
     if wsb == 0:
         raise ValidationError(f"ensemble of {de.n} members is not supported by the tile layout")
     ws = de.workspace(wsb)
-    N.call("pidb_member_masses", de.ptr(), de.dtype_code, de.n, de.m, de.ld, de.wptr(),
+    _launch("pidb_member_masses", de.ptr(), de.dtype_code, de.n, de.m, de.ld, de.wptr(),
            mass.data_ptr(), None if nb is None else nb.data_ptr(), ws.data_ptr(), ws.numel(),
            stream_ptr(dev))
     if de.process_group is not None:
@@ -143,7 +161,7 @@ def _mean_partials(de: DeviceEnsemble) -> torch.Tensor:
         raise ValidationError(f"ensemble of {de.n} members is not supported by the tile layout")
     ws = de.workspace(wsb)
     p = buf.data_ptr()
-    N.call("pidb_pid_mean_partials", de.ptr(), de.dtype_code, de.n, de.m, de.ld, de.wptr(),
+    _launch("pidb_pid_mean_partials", de.ptr(), de.dtype_code, de.n, de.m, de.ld, de.wptr(),
            p, p + 8 * de.n, p + 16 * de.n, ws.data_ptr(), ws.numel(), stream_ptr(dev))
     _allreduce(buf, de)
     return buf
@@ -154,7 +172,7 @@ def _col_sums(de: DeviceEnsemble, inv: torch.Tensor) -> torch.Tensor:
     dev = de.device
     col = _f64(de.n, dev)
     ws = de.workspace(N.load().pidb_pid_mean_workspace_bytes(de.n, de.m, de.dtype_code))
-    N.call("pidb_pid_colsums", de.ptr(), de.dtype_code, de.n, de.m, de.ld, de.wptr(),
+    _launch("pidb_pid_colsums", de.ptr(), de.dtype_code, de.n, de.m, de.ld, de.wptr(),
            inv.data_ptr(), col.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr(dev))
     _allreduce(col, de)
     return col

@@ -106,8 +106,14 @@ class DeviceEnsemble:
         dims: Sequence[int] | None = None,
         validate: bool = True,
         device=None,
+        process_group=None,
+        cell_range: tuple[int, int] | None = None,
     ) -> "DeviceEnsemble":
-        """Stage an (n, *dims) tensor or array (host or device)."""
+        """Stage an (n, *dims) tensor or array (host or device).
+
+        For a multi-GPU job pass this rank's cell slab (n, hi - lo) together
+        with ``process_group`` and ``cell_range=(lo, hi)``; ``dims`` then names
+        the full grid and ``weights`` the slab's weights."""
         if isinstance(values, np.ndarray):
             values = torch.from_numpy(values)
         if values.dim() < 2:
@@ -116,20 +122,32 @@ class DeviceEnsemble:
         if n == 0:
             raise DegenerateEnsembleError("ensemble needs at least one member")
         dims = tuple(int(d) for d in (dims if dims is not None else values.shape[1:]))
-        m = int(np.prod(dims))
+        m = int(np.prod(dims)) if cell_range is None else cell_range[1] - cell_range[0]
         if int(np.prod(values.shape[1:])) != m:
             raise ValidationError(f"member tensor has {values[0].numel()} cells, grid expects {m}")
+        cr = (0, m) if cell_range is None else tuple(cell_range)
         dev = require_cuda(device if device is not None else
                            (values.device if values.is_cuda else None))
         dt = torch.float64 if values.dtype == torch.float64 else torch.float32
-        ld = padded_ld(m)
-        out = torch.zeros((n, ld), dtype=dt, device=dev)
-        out[:, :m].copy_(values.reshape(n, m), non_blocking=values.device.type == "cpu" and values.is_pinned())
-        if validate:
-            _validate_inplace(out[:, :m])
         ids = _make_ids(ids, n)
         w_host, w_dev = _weights(weights, m, dev)
-        return cls(out, m, dims, ids, w_dev, w_host)
+        flat = values.reshape(n, m)
+        es = 8 if dt == torch.float64 else 4
+        if (flat.is_cuda and flat.device == dev and flat.dtype == dt and flat.stride(1) == 1
+                and (flat.stride(0) * es) % 16 == 0 and flat.data_ptr() % 16 == 0):
+            # zero-copy: the caller's device tensor already has a TMA-legal layout
+            de = cls(flat.as_strided((n, flat.stride(0)), (flat.stride(0), 1)), m, dims, ids,
+                     w_dev, w_host, process_group, cr)
+            if validate and _validate(de, clamp=False):
+                de = cls(_copy_padded(flat, dt, dev), m, dims, ids, w_dev, w_host, process_group, cr)
+                _validate(de, clamp=True)
+            return de
+        if flat.dtype != dt:
+            flat = flat.to(dt)
+        de = cls(_copy_padded(flat, dt, dev), m, dims, ids, w_dev, w_host, process_group, cr)
+        if validate:
+            _validate(de, clamp=True)
+        return de
 
     @classmethod
     def from_masks(cls, masks: Sequence, ids=None, device=None) -> "DeviceEnsemble":
@@ -191,16 +209,44 @@ def _weights(weights, m, dev, lo: int = 0, hi: int | None = None):
     return w_host, w_dev
 
 
-def _validate_inplace(v: torch.Tensor) -> None:
-    """ProbMask value policy (grid.py:105-116) for raw tensors: finite, within
-    [0,1] up to VALUE_TOLERANCE, clamped."""
-    if not bool(torch.isfinite(v).all()):
+def _copy_padded(flat: torch.Tensor, dt, dev) -> torch.Tensor:
+    """(n, m) tensor (host or device) -> zero-padded (n, ld) device matrix,
+    one pitched copy (pidb_copy_rows)."""
+    n, m = flat.shape
+    ld = padded_ld(m)
+    out = torch.empty((n, ld), dtype=dt, device=dev)
+    if ld > m:
+        out[:, m:].zero_()
+    src = flat if flat.stride(1) == 1 else flat.contiguous()
+    es = out.element_size()
+    N.call("pidb_copy_rows", out.data_ptr(), ld * es, src.data_ptr(), src.stride(0) * es,
+           m * es, n, stream_ptr(dev))
+    if not src.is_cuda and not src.is_pinned():
+        torch.cuda.current_stream(dev).synchronize()  # pageable source must outlive the copy
+    return out
+
+
+def _key_to_double(k: int) -> float:
+    import struct
+
+    b = k if k >= 0 else k ^ 0x7FFFFFFFFFFFFFFF
+    return struct.unpack("<d", struct.pack("<q", b))[0]
+
+
+def _validate(de: "DeviceEnsemble", clamp: bool) -> bool:
+    """ProbMask value policy (grid.py:105-116) on the device.  Raises for
+    non-finite or out-of-tolerance values; returns True when values needed
+    clipping (done in place when ``clamp``)."""
+    stats = torch.empty(3, dtype=torch.int64, device=de.device)
+    N.call("pidb_validate", de.ptr(), de.dtype_code, de.n, de.m, de.ld, int(clamp),
+           stats.data_ptr(), stream_ptr(de.device))
+    nf, kmin, kmax = (int(v) for v in stats.cpu().tolist())
+    if nf:
         raise ValidationError("mask values must be finite")
-    lo, hi = float(v.min()), float(v.max())
+    lo, hi = _key_to_double(kmin), _key_to_double(kmax)
     if lo < -VALUE_TOLERANCE or hi > 1.0 + VALUE_TOLERANCE:
         raise ValidationError(f"mask values outside [0, 1]: min={lo!r} max={hi!r}")
-    if lo < 0.0 or hi > 1.0:
-        v.clamp_(0.0, 1.0)
+    return lo < 0.0 or hi > 1.0
 
 
 class _PinnedRing:

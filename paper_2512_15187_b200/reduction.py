@@ -39,7 +39,9 @@ def gram_device(de: DeviceEnsemble) -> torch.Tensor:
     g = torch.empty((de.n, de.n), dtype=torch.float64, device=de.device)
     wsb = lib.pidb_gram_tf32x3_workspace_bytes(de.n, de.m)
     ws = de.workspace(wsb)
-    N.call("pidb_gram_tf32x3", de.ptr(), de.n, de.m, de.ld, de.wptr(), g.data_ptr(),
+    from .depth import _launch
+
+    _launch("pidb_gram_tf32x3", de.ptr(), de.n, de.m, de.ld, de.wptr(), g.data_ptr(),
            ws.data_ptr(), ws.numel(), stream_ptr(de.device))
     _allreduce(g, de)
     return g
@@ -60,7 +62,9 @@ def intersection_gram(de: DeviceEnsemble) -> torch.Tensor:
     b = pack_binary(de)
     g = torch.empty((de.n, de.n), dtype=torch.int64, device=de.device)
     ws = de.workspace(lib.pidb_gram_i8_workspace_bytes(de.n, de.m))
-    N.call("pidb_gram_i8", b.data_ptr(), de.n, de.m, b.stride(0), g.data_ptr(),
+    from .depth import _launch
+
+    _launch("pidb_gram_i8", b.data_ptr(), de.n, de.m, b.stride(0), g.data_ptr(),
            ws.data_ptr(), ws.numel(), stream_ptr(de.device))
     _allreduce(g, de)
     return g
