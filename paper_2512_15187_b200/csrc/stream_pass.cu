@@ -25,7 +25,10 @@
 namespace pidb {
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef PIDB_K5_THREADS
+#define PIDB_K5_THREADS 512
+#endif
+constexpr int kThreads = PIDB_K5_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int MODE_MEAN = 0;
 constexpr int MODE_COLS = 1;
@@ -49,68 +52,74 @@ struct StreamParams {
   int64_t* out_nb;        // n (MODE_MASS, nullable)
 };
 
-template <int LB>
-__device__ __forceinline__ uint32_t swz(uint32_t off) {
-  constexpr uint32_t mask = LB == 128 ? 7u : (LB == 64 ? 3u : 1u);
-  return off ^ (((off >> 7) & mask) << 4);
-}
-
 template <typename T>
-struct Chunk;
+struct Vec;  // one 16-byte chunk of member values
 template <>
-struct Chunk<float> {
+struct Vec<float> {
   static constexpr int EPC = 4;
-  __device__ static void load(const char* p, double (&v)[4]) {
-    float4 f = *reinterpret_cast<const float4*>(p);
+  __device__ static void load(const unsigned char* p, double (&v)[4]) {
+    const float4 f = *reinterpret_cast<const float4*>(p);
     v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
   }
-  __device__ static void loadf(const char* p, float (&v)[4]) {
-    float4 f = *reinterpret_cast<const float4*>(p);
-    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  __device__ static float4 loadf(const unsigned char* p) {
+    return *reinterpret_cast<const float4*>(p);
   }
 };
 template <>
-struct Chunk<double> {
+struct Vec<double> {
   static constexpr int EPC = 2;
-  __device__ static void load(const char* p, double (&v)[2]) {
-    double2 f = *reinterpret_cast<const double2*>(p);
+  __device__ static void load(const unsigned char* p, double (&v)[2]) {
+    const double2 f = *reinterpret_cast<const double2*>(p);
     v[0] = f.x; v[1] = f.y;
   }
 };
 
 __device__ __forceinline__ bool is_nonbinary(double x) { return !(x == 0.0 || x == 1.0); }
 
+// XOR applied to the 16-byte chunk index of line `r` by the TMA swizzle
+// (rows of one column box are consecutive lines, boxes are 8-line aligned).
+template <int LB>
+__device__ __forceinline__ uint32_t swz_xor(uint32_t r) {
+  if constexpr (LB == 128) return r & 7u;
+  else if constexpr (LB == 64) return (r >> 1) & 3u;
+  else return (r >> 2) & 1u;
+}
+
 // LB: bytes per smem line (box inner extent, = swizzle span); NCB column boxes
 // per tile; IPT items (column box, member) per thread.
 template <typename T, int LB, int NCB, int IPT>
 __global__ void __launch_bounds__(kThreads, 1)
     stream_pass_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
-  constexpr int EPC = Chunk<T>::EPC;            // elements per 16-byte chunk
+  constexpr int EPC = Vec<T>::EPC;              // elements per 16-byte chunk
   constexpr int E = LB / (int)sizeof(T);        // elements per line (box inner)
   constexpr int V = NCB * E;                    // cells per tile
   constexpr int CPL = LB / 16;                  // chunks per line
   constexpr int QC = NCB * CPL;                 // chunks per tile row
   constexpr int P = kThreads / QC;              // row phases in pass 1
-  static_assert(kThreads % QC == 0, "layout");
+  constexpr int WPH = 32 / QC;                  // row phases inside one warp
+  static_assert(kThreads % QC == 0 && QC <= 32 && P % 8 == 0, "layout");
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* tiles = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // dynamic smem base rounded up to 1024 B (swizzle atom) without leaving the
+  // shared address space (keeps LDS instead of generic loads)
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  unsigned char* tiles = smem_raw + pad;
   unsigned char* tail = tiles + (size_t)p.stages * p.stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(tail);
-  double* sS = reinterpret_cast<double*>(tail + 8 * 8);     // V: w*S (or w*T)
-  double* sW = sS + V;                                       // V: w
-  double* red = sW + V;                                      // kWarps*V
-  __shared__ unsigned s_ticket;
-  __shared__ double s_col[kWarps];
+  double* sS = reinterpret_cast<double*>(tail + 64);     // V: w*S (or w*T)
+  double* sW = sS + V;                                     // V: w
+  double* red = sW + V;                                    // kWarps*V
+  unsigned* s_ticket = reinterpret_cast<unsigned*>(red + kWarps * V);
+  double* s_col = reinterpret_cast<double*>(s_ticket + 2);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int64_t n = p.n;
+  const int n = (int)p.n;
   const int G = gridDim.x;
   const bool weighted = p.w != nullptr;
   const int mode = p.mode;
-  const int64_t items = (int64_t)NCB * n;
+  const int items = NCB * n;
+  const int cb_rows = p.nrb * p.boxr;  // lines per column box
 
   const int64_t my_tiles = p.tiles > blockIdx.x ? (p.tiles - 1 - blockIdx.x) / G + 1 : 0;
   const uint64_t pol = policy_evict_first();
@@ -135,53 +144,63 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0)
     for (int64_t j = 0; j < my_tiles && j < p.stages; ++j) issue(j);
 
+  // pass-2 items owned by this thread for the whole kernel: item = cb*n + r
+  uint32_t it_line[IPT];  // byte offset of the item's line inside a stage
+  uint32_t it_xor[IPT];   // swizzle XOR of that line
+  int it_vb[IPT];         // first cell of the item's column box
   double acc_row[IPT], acc_mass[IPT];
   int64_t acc_nb[IPT];
 #pragma unroll
-  for (int k = 0; k < IPT; ++k) { acc_row[k] = 0.0; acc_mass[k] = 0.0; acc_nb[k] = 0; }
+  for (int k = 0; k < IPT; ++k) {
+    const int it = tid + k * kThreads;
+    const int cb = it < items ? it / n : 0;
+    const int r = it < items ? it - cb * n : 0;
+    it_line[k] = (uint32_t)((cb * cb_rows + r) * LB);
+    it_xor[k] = swz_xor<LB>((uint32_t)r);
+    it_vb[k] = cb * E;
+    acc_row[k] = 0.0; acc_mass[k] = 0.0; acc_nb[k] = 0;
+  }
   double col_acc = 0.0;
 
-  // pass-1 thread coordinates
+  // pass-1 coordinates: chunk column q (cb, ch), row phase ph; the swizzle
+  // XOR of rows ph, ph+P, ... is constant because P is a multiple of 8.
   const int q = tid % QC, ph = tid / QC;
   const int q_cb = q / CPL, q_ch = q % CPL;
+  const uint32_t p1_off = (uint32_t)((q_cb * cb_rows + ph) * LB) +
+                          ((q_ch ^ swz_xor<LB>((uint32_t)ph)) << 4);
 
   for (int64_t j = 0; j < my_tiles; ++j) {
     const int s = (int)(j % p.stages);
-    const int64_t tile = blockIdx.x + j * G;
-    const int64_t x0 = tile * V;
+    const int64_t x0 = (blockIdx.x + j * G) * (int64_t)V;
     const unsigned char* st = tiles + (size_t)s * p.stage_bytes;
     mbar_wait(&full[s], (uint32_t)((j / p.stages) & 1));
 
     if (mode != MODE_MASS) {
       // ------------------------------------------------ pass 1: column sums
       double part[EPC];
+      const unsigned char* pa = st + p1_off;
       if constexpr (sizeof(T) == 4) {
         if (mode == MODE_MEAN) {
           float sh[EPC], sc[EPC];
 #pragma unroll
           for (int e = 0; e < EPC; ++e) { sh[e] = 1.0f; sc[e] = 0.0f; }
-          for (int r = ph; r < n; r += P) {
-            const int rb = r / p.boxr, rr = r - rb * p.boxr;
-            const uint32_t off = (uint32_t)(rr * LB + q_ch * 16);
-            float v[4];
-            Chunk<float>::loadf(reinterpret_cast<const char*>(st) +
-                                    (size_t)(q_cb * p.nrb + rb) * p.boxr * LB + swz<LB>(off),
-                                v);
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) fast2sum_acc(sh[e], sc[e], v[e]);
+#pragma unroll 4
+          for (int r = ph; r < n; r += P, pa += P * LB) {
+            const float4 v = Vec<float>::loadf(pa);
+            fast2sum_acc(sh[0], sc[0], v.x);
+            fast2sum_acc(sh[1], sc[1], v.y);
+            fast2sum_acc(sh[2], sc[2], v.z);
+            fast2sum_acc(sh[3], sc[3], v.w);
           }
 #pragma unroll
           for (int e = 0; e < EPC; ++e) part[e] = ((double)sh[e] - 1.0) + (double)sc[e];
         } else {
 #pragma unroll
           for (int e = 0; e < EPC; ++e) part[e] = 0.0;
-          for (int r = ph; r < n; r += P) {
-            const int rb = r / p.boxr, rr = r - rb * p.boxr;
-            const uint32_t off = (uint32_t)(rr * LB + q_ch * 16);
+#pragma unroll 4
+          for (int r = ph; r < n; r += P, pa += P * LB) {
             double v[EPC];
-            Chunk<T>::load(reinterpret_cast<const char*>(st) +
-                               (size_t)(q_cb * p.nrb + rb) * p.boxr * LB + swz<LB>(off),
-                           v);
+            Vec<T>::load(pa, v);
             const double iv = p.inv[r];
 #pragma unroll
             for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
@@ -190,39 +209,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
 #pragma unroll
         for (int e = 0; e < EPC; ++e) part[e] = 0.0;
-        for (int r = ph; r < n; r += P) {
-          const int rb = r / p.boxr, rr = r - rb * p.boxr;
-          const uint32_t off = (uint32_t)(rr * LB + q_ch * 16);
+#pragma unroll 4
+        for (int r = ph; r < n; r += P, pa += P * LB) {
           double v[EPC];
-          Chunk<T>::load(reinterpret_cast<const char*>(st) +
-                             (size_t)(q_cb * p.nrb + rb) * p.boxr * LB + swz<LB>(off),
-                         v);
+          Vec<T>::load(pa, v);
           const double iv = mode == MODE_MEAN ? 1.0 : p.inv[r];
 #pragma unroll
           for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
         }
       }
-      // combine row phases inside the warp (lanes sharing q), fixed tree order
-      if constexpr (QC < 32) {
+      // combine the row phases of this warp (lanes sharing q), fixed order
 #pragma unroll
-        for (int o = QC; o < 32; o <<= 1)
+      for (int o = QC; o < 32; o <<= 1)
 #pragma unroll
-          for (int e = 0; e < EPC; ++e) part[e] += __shfl_xor_sync(0xffffffffu, part[e], o);
-        if (lane < QC) {
+        for (int e = 0; e < EPC; ++e) part[e] += __shfl_xor_sync(0xffffffffu, part[e], o);
+      if (lane < QC) {
 #pragma unroll
-          for (int e = 0; e < EPC; ++e) red[warp * V + q * EPC + e] = part[e];
-        }
-      } else {
-        // QC >= 32: every lane owns distinct cells; phases live in different warps
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) red[ph * V + q * EPC + e] = part[e];
+        for (int e = 0; e < EPC; ++e) red[warp * V + q * EPC + e] = part[e];
       }
       __syncthreads();
-      constexpr int NPH = QC < 32 ? kWarps : P;
       for (int v = tid; v < V; v += kThreads) {
         double S = 0.0;
 #pragma unroll
-        for (int k = 0; k < NPH; ++k) S += red[k * V + v];
+        for (int k = 0; k < kWarps; ++k) S += red[k * V + v];
         const int64_t x = x0 + v;
         const double wx = x < p.m ? (weighted ? p.w[x] : 1.0) : 0.0;
         sS[v] = wx * S;
@@ -240,45 +249,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     // -------------------------------------------------- pass 2: row sweep
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
-      const int64_t it = tid + (int64_t)k * kThreads;
-      if (it < items) {
-        const int cb = (int)(it / n);
-        const int r = (int)(it - (int64_t)cb * n);
-        const int rb = r / p.boxr, rr = r - rb * p.boxr;
-        const char* line = reinterpret_cast<const char*>(st) +
-                           (size_t)(cb * p.nrb + rb) * p.boxr * LB;
-        double ar = acc_row[k], am = acc_mass[k];
+      if (tid + k * kThreads < items) {
+        const unsigned char* line = st + it_line[k];
+        const double* S = sS + it_vb[k];
+        const double* W = sW + it_vb[k];
+        double ar[EPC], am[EPC];
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) { ar[e] = 0.0; am[e] = 0.0; }
         int64_t nb = 0;
 #pragma unroll
         for (int L = 0; L < CPL; ++L) {
           double v[EPC];
-          Chunk<T>::load(line + swz<LB>((uint32_t)(rr * LB + L * 16)), v);
-          const int vb = cb * E + L * EPC;
+          Vec<T>::load(line + ((L ^ it_xor[k]) << 4), v);
+          const int vb = L * EPC;
           if (mode == MODE_MASS) {
 #pragma unroll
             for (int e = 0; e < EPC; ++e) {
-              am = fma(v[e], sW[vb + e], am);
+              am[e] = fma(v[e], W[vb + e], am[e]);
               nb += is_nonbinary(v[e]);
             }
           } else if (mode == MODE_COLS) {
 #pragma unroll
-            for (int e = 0; e < EPC; ++e) ar = fma(v[e], sS[vb + e], ar);
+            for (int e = 0; e < EPC; ++e) ar[e] = fma(v[e], S[vb + e], ar[e]);
           } else if (weighted) {
 #pragma unroll
             for (int e = 0; e < EPC; ++e) {
-              ar = fma(v[e], sS[vb + e], ar);
-              am = fma(v[e], sW[vb + e], am);
+              ar[e] = fma(v[e], S[vb + e], ar[e]);
+              am[e] = fma(v[e], W[vb + e], am[e]);
             }
           } else {
 #pragma unroll
             for (int e = 0; e < EPC; ++e) {
-              ar = fma(v[e], sS[vb + e], ar);
-              am += v[e];
+              ar[e] = fma(v[e], S[vb + e], ar[e]);
+              am[e] += v[e];
             }
           }
         }
-        acc_row[k] = ar;
-        acc_mass[k] = am;
+        double tr = ar[0], tm = am[0];
+#pragma unroll
+        for (int e = 1; e < EPC; ++e) { tr += ar[e]; tm += am[e]; }
+        acc_row[k] += tr;
+        acc_mass[k] += tm;
         acc_nb[k] += nb;
       }
     }
@@ -289,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ------------------------------------------------ CTA partials -> global
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
-    const int64_t it = tid + (int64_t)k * kThreads;
+    const int it = tid + k * kThreads;
     if (it < items) {
       double* dst = p.part + ((size_t)blockIdx.x * items + it) * 2;
       dst[0] = acc_row[k];
@@ -297,27 +308,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   if (p.mode == MODE_MASS && p.part_nb != nullptr) {
-    // merge column boxes of the same member (fixed order) into [grid][n]
+    // integers: merge the column boxes of one member exactly, any order
     int64_t* nbp = p.part_nb + (size_t)blockIdx.x * n;
-    // items with cb==0 own row r; other cb items add in order via smem-free
-    // two-phase write: first cb==0 writes, sync, then cb>0 atomically add
-    // (integers: order-independent, exact).
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
-      const int64_t it = tid + (int64_t)k * kThreads;
+      const int it = tid + k * kThreads;
       if (it < n) nbp[it] = acc_nb[k];
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
-      const int64_t it = tid + (int64_t)k * kThreads;
+      const int it = tid + k * kThreads;
       if (it >= n && it < items)
         atomicAdd(reinterpret_cast<unsigned long long*>(&nbp[it % n]),
                   (unsigned long long)acc_nb[k]);
     }
   }
   {
-    double c = warp_sum(col_acc);
+    const double c = warp_sum(col_acc);
     if (lane == 0) s_col[warp] = c;
     __syncthreads();
     if (tid == 0) {
@@ -328,18 +336,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_ticket = atomicAdd(p.counter, 1u);
+  if (tid == 0) *s_ticket = atomicAdd(p.counter, 1u);
   __syncthreads();
-  if (s_ticket != (unsigned)(G - 1)) return;
+  if (*s_ticket != (unsigned)(G - 1)) return;
 
   // ------------------------------------------- last CTA: fixed-order reduce
   __threadfence();
-  for (int64_t r = warp; r < n; r += kWarps) {
+  for (int r = warp; r < n; r += kWarps) {
     double a = 0.0, b = 0.0;
     int64_t nb = 0;
     for (int g = lane; g < G; g += 32) {
       for (int cb = 0; cb < NCB; ++cb) {
-        const double* src = p.part + ((size_t)g * items + (int64_t)cb * n + r) * 2;
+        const double* src = p.part + ((size_t)g * items + cb * n + r) * 2;
         a += __ldcg(src);
         b += __ldcg(src + 1);
       }
@@ -379,7 +387,7 @@ struct Plan {
 
 constexpr size_t kSmemBudget = 227 * 1024;
 
-size_t tail_bytes(int V) { return 64 + (size_t)V * 8 * 2 + (size_t)kWarps * V * 8 + 64; }
+size_t tail_bytes(int V) { return 64 + (size_t)V * 8 * 2 + (size_t)kWarps * V * 8 + 16 + kWarps * 8 + 64; }
 
 bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
   if (n < 1 || m < 1) return false;
@@ -398,7 +406,7 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
     const int64_t items = (int64_t)c.ncb * n;
     int ipt = 1;
     while ((int64_t)ipt * kThreads < items) ipt *= 2;
-    if (ipt > 16) return false;
+    if (ipt > (c.lb == 128 ? 2 : (c.lb == 64 ? 4 : 8))) continue;
     pl.lb = c.lb; pl.ncb = c.ncb; pl.ipt = ipt; pl.boxr = boxr_full; pl.nrb = nrb;
     pl.stages = stages; pl.stage_bytes = sb;
     pl.smem = (size_t)stages * sb + tb;
@@ -429,14 +437,15 @@ int launch_t(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream
 
 template <typename T, int LB, int NCB>
 int launch_ipt(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream_t st) {
+  // only the (layout, items-per-thread) pairs make_plan can produce are built
+  constexpr int kMaxIpt = LB == 128 ? 2 : (LB == 64 ? 4 : 8);
   switch (pl.ipt) {
     case 1: return launch_t<T, LB, NCB, 1>(tm, sp, pl, st);
     case 2: return launch_t<T, LB, NCB, 2>(tm, sp, pl, st);
-    case 4: return launch_t<T, LB, NCB, 4>(tm, sp, pl, st);
-    case 8: return launch_t<T, LB, NCB, 8>(tm, sp, pl, st);
-    case 16: return launch_t<T, LB, NCB, 16>(tm, sp, pl, st);
+    case 4: if constexpr (kMaxIpt >= 4) return launch_t<T, LB, NCB, 4>(tm, sp, pl, st); break;
+    case 8: if constexpr (kMaxIpt >= 8) return launch_t<T, LB, NCB, 8>(tm, sp, pl, st); break;
   }
-  set_error("unsupported items-per-thread %d", pl.ipt);
+  set_error("unsupported items-per-thread %d for %d-byte lines", pl.ipt, LB);
   return PIDB_EUNSUPPORTED;
 }
 
