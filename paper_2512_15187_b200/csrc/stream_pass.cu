@@ -85,9 +85,22 @@ __device__ __forceinline__ uint32_t swz_xor(uint32_t r) {
   else return (r >> 2) & 1u;
 }
 
-// LB: bytes per smem line (box inner extent, = swizzle span); NCB column boxes
-// per tile; IPT items (column box, member) per thread.
-template <typename T, int LB, int NCB, int IPT>
+// ---------------------------------------------------------------------------
+// Kernel structure (software-pipelined over tiles, ONE block barrier per tile):
+//   iteration j:  wait TMA(tile j)
+//                 pass 1(tile j): column partials -> red[]          (all threads)
+//                 __syncthreads
+//                 refill: TMA(tile j-2+stages) into the stage tile j-2 used
+//                 finalize(tile j): S, w*S, w -> sS/sW[j&1]          (V threads)
+//                 pass 2(tile j-1): row sums against sS/sW[(j-1)&1]  (all threads)
+// so finalize and pass 2 overlap other warps' work instead of serialising
+// behind two barriers.  Pass 2 has two register layouts:
+//   ROWS>0 : (128-byte lines, 2 column boxes) lane l owns 8 bytes of the row's
+//            64-cell tile slice (lanes 0-15 box 0, 16-31 box 1), warp w owns
+//            rows w, w+W, ..., accumulators stay in registers for the whole
+//            kernel and are reduced across lanes once at the end;
+//   ROWS==0: thread owns (column box, member) items (large N), IPT per thread.
+template <typename T, int LB, int NCB, int IPT, int ROWS>
 __global__ void __launch_bounds__(kThreads, 1)
     stream_pass_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
   constexpr int EPC = Vec<T>::EPC;              // elements per 16-byte chunk
@@ -96,8 +109,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int CPL = LB / 16;                  // chunks per line
   constexpr int QC = NCB * CPL;                 // chunks per tile row
   constexpr int P = kThreads / QC;              // row phases in pass 1
-  constexpr int WPH = 32 / QC;                  // row phases inside one warp
+  constexpr int EPL = 8 / (int)sizeof(T);       // elements per lane in ROWS pass 2
   static_assert(kThreads % QC == 0 && QC <= 32 && P % 8 == 0, "layout");
+  static_assert(ROWS == 0 || (LB == 128 && NCB == 2), "row-resident pass 2 needs 2x128B lines");
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // dynamic smem base rounded up to 1024 B (swizzle atom) without leaving the
@@ -106,10 +120,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* tiles = smem_raw + pad;
   unsigned char* tail = tiles + (size_t)p.stages * p.stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(tail);
-  double* sS = reinterpret_cast<double*>(tail + 64);     // V: w*S (or w*T)
-  double* sW = sS + V;                                     // V: w
-  double* red = sW + V;                                    // kWarps*V
-  unsigned* s_ticket = reinterpret_cast<unsigned*>(red + kWarps * V);
+  double* sS = reinterpret_cast<double*>(tail + 64);     // [2][V]: w*S (or w*T)
+  double* sW = sS + 2 * V;                                 // [2][V]: w
+  double* red = sW + 2 * V;                                // [2][kWarps][V]
+  unsigned* s_ticket = reinterpret_cast<unsigned*>(red + 2 * kWarps * V);
   double* s_col = reinterpret_cast<double*>(s_ticket + 2);
 
   const int tid = threadIdx.x;
@@ -144,21 +158,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0)
     for (int64_t j = 0; j < my_tiles && j < p.stages; ++j) issue(j);
 
-  // pass-2 items owned by this thread for the whole kernel: item = cb*n + r
-  uint32_t it_line[IPT];  // byte offset of the item's line inside a stage
-  uint32_t it_xor[IPT];   // swizzle XOR of that line
-  int it_vb[IPT];         // first cell of the item's column box
-  double acc_row[IPT], acc_mass[IPT];
-  int64_t acc_nb[IPT];
+  // ------------------------------------------------------ pass-2 state
+  constexpr int NACC = ROWS > 0 ? ROWS : IPT;
+  double acc_row[NACC], acc_mass[NACC];
+  int acc_nb[NACC];
 #pragma unroll
-  for (int k = 0; k < IPT; ++k) {
-    const int it = tid + k * kThreads;
-    const int cb = it < items ? it / n : 0;
-    const int r = it < items ? it - cb * n : 0;
-    it_line[k] = (uint32_t)((cb * cb_rows + r) * LB);
-    it_xor[k] = swz_xor<LB>((uint32_t)r);
-    it_vb[k] = cb * E;
-    acc_row[k] = 0.0; acc_mass[k] = 0.0; acc_nb[k] = 0;
+  for (int k = 0; k < NACC; ++k) { acc_row[k] = 0.0; acc_mass[k] = 0.0; acc_nb[k] = 0; }
+  // ROWS layout: lane -> (column box, 8-byte slot) of every owned row
+  const int r_cb = lane >> 4, r_pos = lane & 15;
+  const int r_cell = r_cb * E + r_pos * EPL;  // first tile cell of this lane
+  // ITEMS layout: item = cb*n + r, fixed per thread
+  uint32_t it_line[ROWS > 0 ? 1 : IPT];
+  uint32_t it_xor[ROWS > 0 ? 1 : IPT];
+  int it_vb[ROWS > 0 ? 1 : IPT];
+  if constexpr (ROWS == 0) {
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int it = tid + k * kThreads;
+      const int cb = it < items ? it / n : 0;
+      const int r = it < items ? it - cb * n : 0;
+      it_line[k] = (uint32_t)((cb * cb_rows + r) * LB);
+      it_xor[k] = swz_xor<LB>((uint32_t)r);
+      it_vb[k] = cb * E;
+    }
   }
   double col_acc = 0.0;
 
@@ -169,43 +191,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t p1_off = (uint32_t)((q_cb * cb_rows + ph) * LB) +
                           ((q_ch ^ swz_xor<LB>((uint32_t)ph)) << 4);
 
-  for (int64_t j = 0; j < my_tiles; ++j) {
-    const int s = (int)(j % p.stages);
-    const int64_t x0 = (blockIdx.x + j * G) * (int64_t)V;
-    const unsigned char* st = tiles + (size_t)s * p.stage_bytes;
-    mbar_wait(&full[s], (uint32_t)((j / p.stages) & 1));
-
-    if (mode != MODE_MASS) {
-      // ------------------------------------------------ pass 1: column sums
-      double part[EPC];
-      const unsigned char* pa = st + p1_off;
-      if constexpr (sizeof(T) == 4) {
-        if (mode == MODE_MEAN) {
-          float sh[EPC], sc[EPC];
+  // ------------------------------------------------------ the two passes
+  auto pass1 = [&](const unsigned char* st, double* red) {
+    double part[EPC];
+    const unsigned char* pa = st + p1_off;
+    if constexpr (sizeof(T) == 4) {
+      if (mode == MODE_MEAN) {
+        float sh[EPC], sc[EPC];
 #pragma unroll
-          for (int e = 0; e < EPC; ++e) { sh[e] = 1.0f; sc[e] = 0.0f; }
+        for (int e = 0; e < EPC; ++e) { sh[e] = 1.0f; sc[e] = 0.0f; }
 #pragma unroll 4
-          for (int r = ph; r < n; r += P, pa += P * LB) {
-            const float4 v = Vec<float>::loadf(pa);
-            fast2sum_acc(sh[0], sc[0], v.x);
-            fast2sum_acc(sh[1], sc[1], v.y);
-            fast2sum_acc(sh[2], sc[2], v.z);
-            fast2sum_acc(sh[3], sc[3], v.w);
-          }
-#pragma unroll
-          for (int e = 0; e < EPC; ++e) part[e] = ((double)sh[e] - 1.0) + (double)sc[e];
-        } else {
-#pragma unroll
-          for (int e = 0; e < EPC; ++e) part[e] = 0.0;
-#pragma unroll 4
-          for (int r = ph; r < n; r += P, pa += P * LB) {
-            double v[EPC];
-            Vec<T>::load(pa, v);
-            const double iv = p.inv[r];
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
-          }
+        for (int r = ph; r < n; r += P, pa += P * LB) {
+          const float4 v = Vec<float>::loadf(pa);
+          fast2sum_acc(sh[0], sc[0], v.x);
+          fast2sum_acc(sh[1], sc[1], v.y);
+          fast2sum_acc(sh[2], sc[2], v.z);
+          fast2sum_acc(sh[3], sc[3], v.w);
         }
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) part[e] = ((double)sh[e] - 1.0) + (double)sc[e];
       } else {
 #pragma unroll
         for (int e = 0; e < EPC; ++e) part[e] = 0.0;
@@ -213,115 +217,187 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int r = ph; r < n; r += P, pa += P * LB) {
           double v[EPC];
           Vec<T>::load(pa, v);
-          const double iv = mode == MODE_MEAN ? 1.0 : p.inv[r];
+          const double iv = __ldg(p.inv + r);
 #pragma unroll
           for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
         }
       }
-      // combine the row phases of this warp (lanes sharing q), fixed order
+    } else {
 #pragma unroll
-      for (int o = QC; o < 32; o <<= 1)
+      for (int e = 0; e < EPC; ++e) part[e] = 0.0;
+#pragma unroll 4
+      for (int r = ph; r < n; r += P, pa += P * LB) {
+        double v[EPC];
+        Vec<T>::load(pa, v);
+        const double iv = mode == MODE_MEAN ? 1.0 : __ldg(p.inv + r);
 #pragma unroll
-        for (int e = 0; e < EPC; ++e) part[e] += __shfl_xor_sync(0xffffffffu, part[e], o);
-      if (lane < QC) {
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) red[warp * V + q * EPC + e] = part[e];
+        for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
       }
-      __syncthreads();
-      for (int v = tid; v < V; v += kThreads) {
+    }
+    // combine the row phases inside this warp (lanes sharing q), fixed order
+#pragma unroll
+    for (int o = QC; o < 32; o <<= 1)
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) part[e] += __shfl_xor_sync(0xffffffffu, part[e], o);
+    if (lane < QC) {
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) red[warp * V + q * EPC + e] = part[e];
+    }
+  };
+
+  auto finalize = [&](int64_t j, int buf) {  // threads < V
+    const double* rd = red + buf * kWarps * V;
+    const int64_t x0 = (blockIdx.x + j * G) * (int64_t)V;
+    for (int v = tid; v < V; v += kThreads) {
+      const int64_t x = x0 + v;
+      const double wx = x < p.m ? (weighted ? __ldg(p.w + x) : 1.0) : 0.0;
+      sW[buf * V + v] = wx;
+      if (mode != MODE_MASS) {
         double S = 0.0;
 #pragma unroll
-        for (int k = 0; k < kWarps; ++k) S += red[k * V + v];
-        const int64_t x = x0 + v;
-        const double wx = x < p.m ? (weighted ? p.w[x] : 1.0) : 0.0;
-        sS[v] = wx * S;
-        sW[v] = wx;
+        for (int k = 0; k < kWarps; ++k) S += rd[k * V + v];
+        sS[buf * V + v] = wx * S;
         col_acc = fma(wx, S, col_acc);
       }
-    } else {
-      for (int v = tid; v < V; v += kThreads) {
-        const int64_t x = x0 + v;
-        sW[v] = x < p.m ? (weighted ? p.w[x] : 1.0) : 0.0;
+    }
+  };
+
+  auto pass2 = [&](const unsigned char* st, int buf) {
+    const double* S = sS + buf * V;
+    const double* W = sW + buf * V;
+    if constexpr (ROWS > 0) {
+      double s_l[EPL], w_l[EPL];
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) { s_l[e] = S[r_cell + e]; w_l[e] = W[r_cell + e]; }
+      const uint32_t lane_off = (uint32_t)(r_cb * cb_rows * LB) + (uint32_t)((r_pos & 1) * 8);
+      const int chunk = r_pos >> 1;
+#define PIDB_ROWS_LOOP(BODY)                                                          \
+  _Pragma("unroll") for (int k = 0; k < ROWS; ++k) {                                  \
+    const int r = warp + k * kWarps;                                                  \
+    if (r < n) {                                                                      \
+      const unsigned char* a = st + lane_off + (uint32_t)(r * LB) +                   \
+                               ((uint32_t)(chunk ^ (r & 7)) << 4);                    \
+      double v[EPL];                                                                  \
+      if constexpr (sizeof(T) == 4) {                                                 \
+        const float2 f = *reinterpret_cast<const float2*>(a);                        \
+        v[0] = f.x; v[EPL - 1] = f.y;                                                 \
+      } else {                                                                        \
+        v[0] = *reinterpret_cast<const double*>(a);                                   \
+      }                                                                               \
+      _Pragma("unroll") for (int e = 0; e < EPL; ++e) { BODY; }                       \
+    }                                                                                 \
+  }
+      if (mode == MODE_MEAN && !weighted) {
+        PIDB_ROWS_LOOP(acc_row[k] = fma(v[e], s_l[e], acc_row[k]); acc_mass[k] += v[e])
+      } else if (mode == MODE_MASS) {
+        PIDB_ROWS_LOOP(acc_mass[k] = fma(v[e], w_l[e], acc_mass[k]); acc_nb[k] += is_nonbinary(v[e]))
+      } else if (mode == MODE_COLS) {
+        PIDB_ROWS_LOOP(acc_row[k] = fma(v[e], s_l[e], acc_row[k]))
+      } else {
+        PIDB_ROWS_LOOP(acc_row[k] = fma(v[e], s_l[e], acc_row[k]);
+                       acc_mass[k] = fma(v[e], w_l[e], acc_mass[k]))
       }
+#undef PIDB_ROWS_LOOP
+    } else {
+#define PIDB_ITEMS_LOOP(BODY)                                                         \
+  _Pragma("unroll") for (int k = 0; k < IPT; ++k) {                                   \
+    if (tid + k * kThreads < items) {                                                 \
+      const unsigned char* line = st + it_line[k];                                    \
+      const double* Sk = S + it_vb[k];                                                \
+      const double* Wk = W + it_vb[k];                                                \
+      double ar[EPC], am[EPC];                                                        \
+      int nb = 0;                                                                     \
+      _Pragma("unroll") for (int e = 0; e < EPC; ++e) { ar[e] = 0.0; am[e] = 0.0; }   \
+      _Pragma("unroll") for (int L = 0; L < CPL; ++L) {                               \
+        double v[EPC];                                                                \
+        Vec<T>::load(line + ((L ^ it_xor[k]) << 4), v);                               \
+        const int vb = L * EPC;                                                       \
+        _Pragma("unroll") for (int e = 0; e < EPC; ++e) { BODY; }                     \
+      }                                                                               \
+      double tr = ar[0], tm = am[0];                                                  \
+      _Pragma("unroll") for (int e = 1; e < EPC; ++e) { tr += ar[e]; tm += am[e]; }   \
+      acc_row[k] += tr;                                                               \
+      acc_mass[k] += tm;                                                              \
+      acc_nb[k] += nb;                                                                \
+    }                                                                                 \
+  }
+      if (mode == MODE_MEAN && !weighted) {
+        PIDB_ITEMS_LOOP(ar[e] = fma(v[e], Sk[vb + e], ar[e]); am[e] += v[e])
+      } else if (mode == MODE_MASS) {
+        PIDB_ITEMS_LOOP(am[e] = fma(v[e], Wk[vb + e], am[e]); nb += is_nonbinary(v[e]))
+      } else if (mode == MODE_COLS) {
+        PIDB_ITEMS_LOOP(ar[e] = fma(v[e], Sk[vb + e], ar[e]))
+      } else {
+        PIDB_ITEMS_LOOP(ar[e] = fma(v[e], Sk[vb + e], ar[e]); am[e] = fma(v[e], Wk[vb + e], am[e]))
+      }
+#undef PIDB_ITEMS_LOOP
+    }
+  };
+
+  // ------------------------------------------------------ pipelined loop
+  int s_cur = 0;        // stage of tile j
+  uint32_t par = 0;     // mbarrier parity of tile j
+  int s_prev = 0;       // stage of tile j-1
+  for (int64_t j = 0; j <= my_tiles; ++j) {
+    const bool have = j < my_tiles;
+    if (have) {
+      mbar_wait(&full[s_cur], par);
+      if (mode != MODE_MASS)
+        pass1(tiles + (size_t)s_cur * p.stage_bytes, red + (j & 1) * kWarps * V);
     }
     __syncthreads();
-
-    // -------------------------------------------------- pass 2: row sweep
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      if (tid + k * kThreads < items) {
-        const unsigned char* line = st + it_line[k];
-        const double* S = sS + it_vb[k];
-        const double* W = sW + it_vb[k];
-        double ar[EPC], am[EPC];
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) { ar[e] = 0.0; am[e] = 0.0; }
-        int64_t nb = 0;
-#pragma unroll
-        for (int L = 0; L < CPL; ++L) {
-          double v[EPC];
-          Vec<T>::load(line + ((L ^ it_xor[k]) << 4), v);
-          const int vb = L * EPC;
-          if (mode == MODE_MASS) {
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) {
-              am[e] = fma(v[e], W[vb + e], am[e]);
-              nb += is_nonbinary(v[e]);
-            }
-          } else if (mode == MODE_COLS) {
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) ar[e] = fma(v[e], S[vb + e], ar[e]);
-          } else if (weighted) {
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) {
-              ar[e] = fma(v[e], S[vb + e], ar[e]);
-              am[e] = fma(v[e], W[vb + e], am[e]);
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) {
-              ar[e] = fma(v[e], S[vb + e], ar[e]);
-              am[e] += v[e];
-            }
-          }
-        }
-        double tr = ar[0], tm = am[0];
-#pragma unroll
-        for (int e = 1; e < EPC; ++e) { tr += ar[e]; tm += am[e]; }
-        acc_row[k] += tr;
-        acc_mass[k] += tm;
-        acc_nb[k] += nb;
-      }
-    }
-    __syncthreads();  // every thread is done with stage s (and sS/sW)
-    if (tid == 0 && j + p.stages < my_tiles) issue(j + p.stages);
+    // tile j-2's stage was last read by pass 2 in the previous iteration
+    if (tid == 0 && j >= 2 && j - 2 + p.stages < my_tiles) issue(j - 2 + p.stages);
+    if (have) finalize(j, (int)(j & 1));
+    if (j >= 1) pass2(tiles + (size_t)s_prev * p.stage_bytes, (int)((j - 1) & 1));
+    s_prev = s_cur;
+    if (++s_cur == p.stages) { s_cur = 0; par ^= 1u; }
   }
 
   // ------------------------------------------------ CTA partials -> global
+  // part layout: [grid][p.part_ncb * n][2]
+  if constexpr (ROWS > 0) {
 #pragma unroll
-  for (int k = 0; k < IPT; ++k) {
-    const int it = tid + k * kThreads;
-    if (it < items) {
-      double* dst = p.part + ((size_t)blockIdx.x * items + it) * 2;
-      dst[0] = acc_row[k];
-      dst[1] = acc_mass[k];
+    for (int k = 0; k < ROWS; ++k) {
+      const int r = warp + k * kWarps;
+      const double a = warp_sum(acc_row[k]);
+      const double b = warp_sum(acc_mass[k]);
+      int nb = acc_nb[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+      if (lane == 0 && r < n) {
+        double* dst = p.part + ((size_t)blockIdx.x * n + r) * 2;
+        dst[0] = a;
+        dst[1] = b;
+        if (p.mode == MODE_MASS && p.part_nb != nullptr) p.part_nb[(size_t)blockIdx.x * n + r] = nb;
+      }
     }
-  }
-  if (p.mode == MODE_MASS && p.part_nb != nullptr) {
-    // integers: merge the column boxes of one member exactly, any order
-    int64_t* nbp = p.part_nb + (size_t)blockIdx.x * n;
+  } else {
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
       const int it = tid + k * kThreads;
-      if (it < n) nbp[it] = acc_nb[k];
+      if (it < items) {
+        double* dst = p.part + ((size_t)blockIdx.x * items + it) * 2;
+        dst[0] = acc_row[k];
+        dst[1] = acc_mass[k];
+      }
     }
-    __syncthreads();
+    if (p.mode == MODE_MASS && p.part_nb != nullptr) {
+      // integers: merge the column boxes of one member exactly, any order
+      int64_t* nbp = p.part_nb + (size_t)blockIdx.x * n;
 #pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      const int it = tid + k * kThreads;
-      if (it >= n && it < items)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&nbp[it % n]),
-                  (unsigned long long)acc_nb[k]);
+      for (int k = 0; k < IPT; ++k) {
+        const int it = tid + k * kThreads;
+        if (it < n) nbp[it] = acc_nb[k];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) {
+        const int it = tid + k * kThreads;
+        if (it >= n && it < items)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&nbp[it % n]),
+                    (unsigned long long)acc_nb[k]);
+      }
     }
   }
   {
@@ -342,12 +418,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ------------------------------------------- last CTA: fixed-order reduce
   __threadfence();
+  constexpr int PNCB = ROWS > 0 ? 1 : NCB;
   for (int r = warp; r < n; r += kWarps) {
     double a = 0.0, b = 0.0;
     int64_t nb = 0;
     for (int g = lane; g < G; g += 32) {
-      for (int cb = 0; cb < NCB; ++cb) {
-        const double* src = p.part + ((size_t)g * items + cb * n + r) * 2;
+      for (int cb = 0; cb < PNCB; ++cb) {
+        const double* src = p.part + ((size_t)g * PNCB * n + cb * n + r) * 2;
         a += __ldcg(src);
         b += __ldcg(src + 1);
       }
@@ -379,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---------------------------------------------------------------- host side
 struct Plan {
-  int lb, ncb, ipt, boxr, nrb, stages, grid;
+  int lb, ncb, ipt, rows, boxr, nrb, stages, grid;
   uint32_t stage_bytes;
   size_t smem;
   int64_t tiles;
@@ -387,7 +464,7 @@ struct Plan {
 
 constexpr size_t kSmemBudget = 227 * 1024;
 
-size_t tail_bytes(int V) { return 64 + (size_t)V * 8 * 2 + (size_t)kWarps * V * 8 + 16 + kWarps * 8 + 64; }
+size_t tail_bytes(int V) { return 64 + (size_t)V * 8 * 4 + (size_t)2 * kWarps * V * 8 + 16 + kWarps * 8 + 64; }
 
 bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
   if (n < 1 || m < 1) return false;
@@ -400,14 +477,21 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
     const int V = c.ncb * c.lb / esize;
     const uint32_t sb = (uint32_t)(c.ncb * rows * c.lb);
     const size_t tb = tail_bytes(V) + 1024;
-    const int min_stages = (c.lb == 32) ? 2 : 3;
+    const int min_stages = 3;  // tiles j (pass 1), j-1 (pass 2) and >= 1 in flight
     int stages = (int)std::min<size_t>(8, (kSmemBudget - tb) / sb);
     if (sb > kSmemBudget || stages < min_stages) continue;
     const int64_t items = (int64_t)c.ncb * n;
     int ipt = 1;
     while ((int64_t)ipt * kThreads < items) ipt *= 2;
     if (ipt > (c.lb == 128 ? 2 : (c.lb == 64 ? 4 : 8))) continue;
-    pl.lb = c.lb; pl.ncb = c.ncb; pl.ipt = ipt; pl.boxr = boxr_full; pl.nrb = nrb;
+    int rows_per_warp = 0;  // row-resident pass 2 for 2x128B-line tiles
+    if (c.lb == 128 && c.ncb == 2) {
+      rows_per_warp = 1;
+      while (rows_per_warp * kWarps < n) rows_per_warp *= 2;
+      if (rows_per_warp > 16) rows_per_warp = 0;
+    }
+    pl.lb = c.lb; pl.ncb = c.ncb; pl.ipt = ipt; pl.rows = rows_per_warp;
+    pl.boxr = boxr_full; pl.nrb = nrb;
     pl.stages = stages; pl.stage_bytes = sb;
     pl.smem = (size_t)stages * sb + tb;
     pl.tiles = (m + V - 1) / V;
@@ -426,9 +510,9 @@ size_t workspace_bytes(const Plan& pl, int64_t n) {
   return b;
 }
 
-template <typename T, int LB, int NCB, int IPT>
+template <typename T, int LB, int NCB, int IPT, int ROWS>
 int launch_t(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream_t st) {
-  auto kern = stream_pass_kernel<T, LB, NCB, IPT>;
+  auto kern = stream_pass_kernel<T, LB, NCB, IPT, ROWS>;
   PIDB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
   kern<<<pl.grid, kThreads, pl.smem, st>>>(tm, sp);
   PIDB_LAUNCH_CHECK("stream_pass_kernel");
@@ -438,12 +522,21 @@ int launch_t(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream
 template <typename T, int LB, int NCB>
 int launch_ipt(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream_t st) {
   // only the (layout, items-per-thread) pairs make_plan can produce are built
+  if constexpr (LB == 128 && NCB == 2) {
+    switch (pl.rows) {
+      case 1: return launch_t<T, LB, NCB, 1, 1>(tm, sp, pl, st);
+      case 2: return launch_t<T, LB, NCB, 1, 2>(tm, sp, pl, st);
+      case 4: return launch_t<T, LB, NCB, 1, 4>(tm, sp, pl, st);
+      case 8: return launch_t<T, LB, NCB, 1, 8>(tm, sp, pl, st);
+      case 16: return launch_t<T, LB, NCB, 1, 16>(tm, sp, pl, st);
+    }
+  }
   constexpr int kMaxIpt = LB == 128 ? 2 : (LB == 64 ? 4 : 8);
   switch (pl.ipt) {
-    case 1: return launch_t<T, LB, NCB, 1>(tm, sp, pl, st);
-    case 2: return launch_t<T, LB, NCB, 2>(tm, sp, pl, st);
-    case 4: if constexpr (kMaxIpt >= 4) return launch_t<T, LB, NCB, 4>(tm, sp, pl, st); break;
-    case 8: if constexpr (kMaxIpt >= 8) return launch_t<T, LB, NCB, 8>(tm, sp, pl, st); break;
+    case 1: return launch_t<T, LB, NCB, 1, 0>(tm, sp, pl, st);
+    case 2: return launch_t<T, LB, NCB, 2, 0>(tm, sp, pl, st);
+    case 4: if constexpr (kMaxIpt >= 4) return launch_t<T, LB, NCB, 4, 0>(tm, sp, pl, st); break;
+    case 8: if constexpr (kMaxIpt >= 8) return launch_t<T, LB, NCB, 8, 0>(tm, sp, pl, st); break;
   }
   set_error("unsupported items-per-thread %d for %d-byte lines", pl.ipt, LB);
   return PIDB_EUNSUPPORTED;
