@@ -114,4 +114,27 @@ __device__ __forceinline__ void fast2sum_acc(float& s, float& c, float x) {
   s = t;
 }
 
+// Packed fp32x2 arithmetic (sm_100 FADD2): two lanes of work per instruction.
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rr;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "add.rn.f32x2 rr, ra, rb;\n\tmov.b64 {%0,%1}, rr;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 ra, rb, rr;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "sub.rn.f32x2 rr, ra, rb;\n\tmov.b64 {%0,%1}, rr;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+// Fast2Sum on two independent (s, c) accumulators at once (s >= 1 >= x).
+__device__ __forceinline__ void fast2sum_acc2(float2& s, float2& c, float2 x) {
+  const float2 t = fadd2(s, x);
+  const float2 z = fsub2(t, s);
+  c = fadd2(c, fsub2(x, z));
+  s = t;
+}
+
 }  // namespace pidb

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int QC = NCB * CPL;                 // chunks per tile row
   constexpr int P = kThreads / QC;              // row phases in pass 1
   constexpr int EPL = 8 / (int)sizeof(T);       // elements per lane in ROWS pass 2
-  static_assert(kThreads % QC == 0 && QC <= 32 && P % 8 == 0, "layout");
+  static_assert(kThreads % QC == 0 && QC <= 32 && P % 8 == 0 && kWarps % 8 == 0, "layout");
   static_assert(ROWS == 0 || (LB == 128 && NCB == 2), "row-resident pass 2 needs 2x128B lines");
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -197,19 +197,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const unsigned char* pa = st + p1_off;
     if constexpr (sizeof(T) == 4) {
       if (mode == MODE_MEAN) {
-        float sh[EPC], sc[EPC];
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) { sh[e] = 1.0f; sc[e] = 0.0f; }
+        float2 sh01 = make_float2(1.0f, 1.0f), sh23 = sh01;
+        float2 sc01 = make_float2(0.0f, 0.0f), sc23 = sc01;
 #pragma unroll 4
         for (int r = ph; r < n; r += P, pa += P * LB) {
           const float4 v = Vec<float>::loadf(pa);
-          fast2sum_acc(sh[0], sc[0], v.x);
-          fast2sum_acc(sh[1], sc[1], v.y);
-          fast2sum_acc(sh[2], sc[2], v.z);
-          fast2sum_acc(sh[3], sc[3], v.w);
+          fast2sum_acc2(sh01, sc01, make_float2(v.x, v.y));
+          fast2sum_acc2(sh23, sc23, make_float2(v.z, v.w));
         }
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) part[e] = ((double)sh[e] - 1.0) + (double)sc[e];
+        part[0] = ((double)sh01.x - 1.0) + (double)sc01.x;
+        part[1] = ((double)sh01.y - 1.0) + (double)sc01.y;
+        part[2] = ((double)sh23.x - 1.0) + (double)sc23.x;
+        part[3] = ((double)sh23.y - 1.0) + (double)sc23.y;
       } else {
 #pragma unroll
         for (int e = 0; e < EPC; ++e) part[e] = 0.0;
@@ -269,14 +268,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       double s_l[EPL], w_l[EPL];
 #pragma unroll
       for (int e = 0; e < EPL; ++e) { s_l[e] = S[r_cell + e]; w_l[e] = W[r_cell + e]; }
-      const uint32_t lane_off = (uint32_t)(r_cb * cb_rows * LB) + (uint32_t)((r_pos & 1) * 8);
-      const int chunk = r_pos >> 1;
+      // rows warp, warp+kWarps, ... share r & 7, hence one swizzled lane offset
+      const unsigned char* lane_base = st + (uint32_t)((r_cb * cb_rows + warp) * LB) +
+                                       ((uint32_t)((r_pos >> 1) ^ (warp & 7)) << 4) +
+                                       (uint32_t)((r_pos & 1) * 8);
 #define PIDB_ROWS_LOOP(BODY)                                                          \
   _Pragma("unroll") for (int k = 0; k < ROWS; ++k) {                                  \
-    const int r = warp + k * kWarps;                                                  \
-    if (r < n) {                                                                      \
-      const unsigned char* a = st + lane_off + (uint32_t)(r * LB) +                   \
-                               ((uint32_t)(chunk ^ (r & 7)) << 4);                    \
+    if (k < ROWS - 1 || warp + k * kWarps < n) {                                      \
+      const unsigned char* a = lane_base + k * (kWarps * LB);                         \
       double v[EPL];                                                                  \
       if constexpr (sizeof(T) == 4) {                                                 \
         const float2 f = *reinterpret_cast<const float2*>(a);                        \
@@ -486,8 +485,7 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
     if (ipt > (c.lb == 128 ? 2 : (c.lb == 64 ? 4 : 8))) continue;
     int rows_per_warp = 0;  // row-resident pass 2 for 2x128B-line tiles
     if (c.lb == 128 && c.ncb == 2) {
-      rows_per_warp = 1;
-      while (rows_per_warp * kWarps < n) rows_per_warp *= 2;
+      rows_per_warp = (int)((n + kWarps - 1) / kWarps);
       if (rows_per_warp > 16) rows_per_warp = 0;
     }
     pl.lb = c.lb; pl.ncb = c.ncb; pl.ipt = ipt; pl.rows = rows_per_warp;
@@ -524,11 +522,12 @@ int launch_ipt(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStre
   // only the (layout, items-per-thread) pairs make_plan can produce are built
   if constexpr (LB == 128 && NCB == 2) {
     switch (pl.rows) {
-      case 1: return launch_t<T, LB, NCB, 1, 1>(tm, sp, pl, st);
-      case 2: return launch_t<T, LB, NCB, 1, 2>(tm, sp, pl, st);
-      case 4: return launch_t<T, LB, NCB, 1, 4>(tm, sp, pl, st);
-      case 8: return launch_t<T, LB, NCB, 1, 8>(tm, sp, pl, st);
-      case 16: return launch_t<T, LB, NCB, 1, 16>(tm, sp, pl, st);
+#define PIDB_ROWS_CASE(R) case R: return launch_t<T, LB, NCB, 1, R>(tm, sp, pl, st);
+      PIDB_ROWS_CASE(1) PIDB_ROWS_CASE(2) PIDB_ROWS_CASE(3) PIDB_ROWS_CASE(4)
+      PIDB_ROWS_CASE(5) PIDB_ROWS_CASE(6) PIDB_ROWS_CASE(7) PIDB_ROWS_CASE(8)
+      PIDB_ROWS_CASE(9) PIDB_ROWS_CASE(10) PIDB_ROWS_CASE(11) PIDB_ROWS_CASE(12)
+      PIDB_ROWS_CASE(13) PIDB_ROWS_CASE(14) PIDB_ROWS_CASE(15) PIDB_ROWS_CASE(16)
+#undef PIDB_ROWS_CASE
     }
   }
   constexpr int kMaxIpt = LB == 128 ? 2 : (LB == 64 ? 4 : 8);
