@@ -1,0 +1,91 @@
+"""Host-side logic of the drop-in (CPU only): containers, validation, error
+types, rank/CV helpers, sharding bounds, and the no-CPU-fallback rule."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2512_15187_b200 as pb
+from conftest import TRIO
+
+
+def test_error_hierarchy():
+    for cls in (pb.ValidationError, pb.GridMismatchError, pb.DegenerateEnsembleError,
+                pb.VolumeFormatError, pb.ManifestError):
+        assert issubclass(cls, pb.FuzzdepthError)
+
+
+def test_gridspec_and_masks_validate_like_the_reference():
+    with pytest.raises(pb.ValidationError):
+        pb.GridSpec((0, 3))
+    with pytest.raises(pb.ValidationError):
+        pb.GridSpec((3,), np.array([1.0, -1.0, 1.0]))
+    g = pb.GridSpec((2, 2))
+    m = pb.ProbMask(g, np.array([[0.0, 1.0 + 5e-10], [-5e-10, 0.5]]))
+    assert m.values.dtype == np.float64 and m.values.max() == 1.0 and m.values.min() == 0.0
+    assert pb.ProbMask(g, np.zeros(4, dtype=np.int32)).values.dtype == np.float32
+    assert not m.values.flags.writeable
+    assert pb.ProbMask(g, np.zeros(4)).values.dtype == np.float64
+    with pytest.raises(pb.ValidationError):
+        pb.ProbMask(g, np.array([0, 0, 0, 1.1]))
+    with pytest.raises(pb.ValidationError):
+        pb.ProbMask(g, np.array([0, 0, np.nan, 1]))
+    with pytest.raises(pb.ValidationError):
+        pb.BinaryMask(g, np.array([0, 2, 0, 1]))
+    with pytest.raises(pb.DegenerateEnsembleError):
+        pb.Ensemble(g, [])
+    with pytest.raises(pb.ValidationError):
+        pb.Ensemble(g, [m, m], ids=["a", "a"])
+    with pytest.raises(pb.GridMismatchError):
+        pb.Ensemble(g, [pb.ProbMask(pb.GridSpec((4,)), np.zeros(4))])
+    e = pb.Ensemble(g, [m, lambda: m])
+    assert e.is_lazy() and len(e.materialize()) == 2
+    assert e.ids == ("member_0000", "member_0001")
+
+
+def test_rank_and_cv_helpers():
+    np.testing.assert_array_equal(pb.ranks_from_depths(np.array([0.5, 0.7, 0.5])), [1, 0, 2])
+    np.testing.assert_array_equal(pb.ranks_from_depths(np.array([0.2, 0.2])), [0, 1])
+    assert pb.mass_cv(np.zeros(3)) == 0.0
+    assert pb.mass_cv(np.array([3.0, 2.0, 1.0])) == pytest.approx(np.sqrt(2 / 3) / 2)
+
+
+def test_depth_result_is_frozen():
+    r = pb.DepthResult(("a", "b"), np.zeros(2), np.zeros(2), np.array([0.1, 0.2]),
+                       np.array([1, 0]), "pid", 0.0, 0.0)
+    assert r.ordered_ids() == ["b", "a"]
+    with pytest.raises(ValueError):
+        r.depth[0] = 1.0
+    with pytest.raises(pb.ValidationError):
+        pb.DepthResult(("a",), np.zeros(2), np.zeros(2), np.zeros(2), np.zeros(2), "pid", 0, 0)
+
+
+def test_workers_contract():
+    with pytest.raises(ValueError):
+        pb.resolve_workers(0)
+    assert pb.resolve_workers(3) == 3
+
+
+@pytest.mark.parametrize("m,world", [(10, 3), (134217728, 8), (7, 8), (65536, 2)])
+def test_shard_bounds_partition(m, world):
+    spans = [pb.shard_bounds(m, r, world) for r in range(world)]
+    assert spans[0][0] == 0 and spans[-1][1] == m
+    for (a, b), (c, d) in zip(spans, spans[1:]):
+        assert b == c and b >= a
+    sizes = [b - a for a, b in spans]
+    assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback():
+    g = pb.GridSpec((4,))
+    e = pb.Ensemble(g, [pb.ProbMask(g, r) for r in TRIO])
+    for fn in (pb.depth_pid, pb.depth_pid_mean, pb.depth_eid):
+        with pytest.raises(RuntimeError, match="no CPU fallback"):
+            fn(e)
+
+
+def test_unknown_method_rejected_before_any_device_work():
+    with pytest.raises(pb.ValidationError):
+        pb.depth_pid(np.zeros((2, 3)), algorithm="bogus")
