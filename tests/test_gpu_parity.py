@@ -44,6 +44,22 @@ def close(got, want, atol):
     np.testing.assert_allclose(got, want, rtol=0, atol=atol)
 
 
+# ------------------------------------------------------------- tensor-core Grams
+
+
+@pytest.mark.parametrize("n,m,density", [(3, 4, 0.5), (8, 25, 0.5), (130, 1000, 0.3),
+                                         (257, 4097, 0.6), (500, 20000, 0.42), (700, 333, 0.9)])
+def test_intersection_gram_exact(pb, n, m, density):
+    """K7 pack + K2 tcgen05 kind::i8 Gram == exact integer counts (bitwise)."""
+    from paper_2512_15187_b200.reduction import intersection_gram
+
+    rng = np.random.default_rng(n * 7 + m)
+    B = (rng.uniform(size=(n, m)) < density).astype(np.float32)
+    de = pb.stage(torch.from_numpy(B))
+    got = intersection_gram(de).cpu().numpy()
+    np.testing.assert_array_equal(got, exact.intersections(B))
+
+
 # ------------------------------------------------------------- golden vectors
 
 
