@@ -388,6 +388,12 @@ def run_e2e(args, host, _, meta, fn, world, pg, dev):
                     "pitched H2D + device validation + K5 + K4 + result D2H"}
 
 
+# cuBLAS TF32 / INT8 dense GEMM peaks measured on this pool's B200 by
+# tools/probe_box.sh (8192^3, best of 20; profiles/r01_probe_box.log).
+TF32_TFLOPS_PROBE = 747.2
+INT8_TOPS_PROBE = 3004.5
+
+
 def run_pid_secondary(args, rank, world, pg, dev, pk):
     import torch
 
@@ -399,30 +405,47 @@ def run_pid_secondary(args, rank, world, pg, dev, pk):
     shard = (rank, world) if world > 1 else None
     de = synth.ellipsoids_device(res, n, 0, 0, device=dev, shard=shard, process_group=pg)
     torch.cuda.synchronize()
-    alg = "gram" if D._gram_available() else "factorized"
-    D.KERNEL_EVENTS = []
-    pb.depth_pid(de, algorithm=alg)
-    D.KERNEL_EVENTS = []
-    ms = timed(lambda: pb.depth_pid(de, algorithm=alg), max(1, min(args.steps, 5)), 2, world)
-    ev = D.KERNEL_EVENTS
-    D.KERNEL_EVENTS = None
     mv = n * res ** 3
-    out = {"workload": "cfg4: PID, 1000 fuzzy ellipsoids 256^3 fp32 (67.1 GB)",
-           "algorithm": alg, "ms_per_depth": ms, "value": mv / (ms * 1e-3),
-           "unit": "member-voxels/s", "pair_voxels_per_s": n * n * res ** 3 / (ms * 1e-3)}
-    if alg == "factorized":
-        k1, _ = kernel_ms(ev, "pidb_pid_mean_partials")
-        k2, _ = kernel_ms(ev, "pidb_pid_colsums")
-        b = n * de.m * 4
-        out["roofline"] = {"bound": "hbm", "achieved": 2 * b / ((k1 + k2) * 1e-3) / 1e9,
-                           "peak": pk["hbm_gbs"], "unit": "GB/s",
-                           "frac": 2 * b / ((k1 + k2) * 1e-3) / 1e9 / pk["hbm_gbs"],
-                           "kernels_ms": [k1, k2], "algorithmic_bytes": 2 * b}
-    else:
-        kg, _ = kernel_ms(ev, "pidb_gram_tf32x3")
-        flops = n * (n + 1) * de.m
-        out["roofline"] = {"bound": "tensor", "achieved": flops / (kg * 1e-3) / 1e12,
-                           "unit": "TFLOP/s", "kernel_ms": kg, "algorithmic_flops": flops}
+    out = {"workload": "cfg4: PID, 1000 fuzzy ellipsoids 256^3 fp32 (67.1 GB)", "unit": "member-voxels/s"}
+    results = {}
+    for alg in ("factorized", "gram"):
+        if alg == "gram" and not D._gram_available():
+            continue
+        D.KERNEL_EVENTS = []
+        results[alg] = pb.depth_pid(de, algorithm=alg)
+        D.KERNEL_EVENTS = []
+        ms = timed(lambda: pb.depth_pid(de, algorithm=alg), max(1, min(args.steps, 5)), 2, world)
+        ev = D.KERNEL_EVENTS
+        D.KERNEL_EVENTS = None
+        o = {"ms_per_depth": ms, "value": mv / (ms * 1e-3),
+             "pair_voxels_per_s": n * n * res ** 3 / (ms * 1e-3)}
+        if alg == "factorized":
+            k1, _ = kernel_ms(ev, "pidb_pid_mean_partials")
+            k2, _ = kernel_ms(ev, "pidb_pid_colsums")
+            b = n * de.m * 4
+            ach = 2 * b / ((k1 + k2) * 1e-3) / 1e9
+            o["roofline"] = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                             "frac": ach / pk["hbm_gbs"], "kernels_ms": [k1, k2],
+                             "algorithmic_bytes": 2 * b, "note": "exact fp64, two HBM passes"}
+        else:
+            kg, _ = kernel_ms(ev, "pidb_gram_tf32x3")
+            flops = n * (n + 1) * de.m  # symmetric Gram, 2 flops per MAC
+            ach = flops / (kg * 1e-3) / 1e12
+            o["roofline"] = {"bound": "tensor", "achieved": ach, "unit": "TFLOP/s",
+                             "peak": TF32_TFLOPS_PROBE / 3,
+                             "frac": ach / (TF32_TFLOPS_PROBE / 3), "kernel_ms": kg,
+                             "algorithmic_flops": flops,
+                             "peak_src": "cuBLAS TF32 probe / 3 (3xTF32 = 3 MMA passes)"}
+        out[alg] = o
+    if len(results) == 2:
+        a, b = results["gram"], results["factorized"]
+        out["gram_vs_exact"] = {
+            "max_rel_depth_err": float(np.abs(a.depth - b.depth).max() / np.abs(b.depth).max()),
+            "rank_mismatches": int(np.sum(a.rank != b.rank)),
+            "min_depth_gap": float(np.min(np.diff(np.sort(b.depth))))}
+    out["ms_per_depth"] = out["factorized"]["ms_per_depth"]
+    out["value"] = out["factorized"]["value"]
+    out["algorithm"] = "factorized (exact, default)"
     del de
     torch.cuda.empty_cache()
     return out

@@ -69,8 +69,6 @@ SIGNATURES: dict[str, tuple] = {
 
 # Entry points declared in pidb.h whose kernels are still being brought up.
 _NOT_YET_BUILT = {
-    "pidb_gram_tf32x3_workspace_bytes",
-    "pidb_gram_tf32x3",
 }
 
 _lib = None

@@ -297,11 +297,13 @@ def _gram_available() -> bool:
 def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") -> DepthResult:
     """Exact probabilistic inclusion depth over all pairs (depth.py:213-228).
 
-    algorithm="gram": the symmetric N x N Gram on tcgen05 (3xTF32, fp64
-    flushes) followed by the fused row/column-sum epilogue — the reference's
-    own formulation.  algorithm="factorized": the exact O(N*M) two-pass
-    identity.  "auto" picks the Gram for float32 ensembles once the kernel is
-    built, the factorisation otherwise.
+    algorithm="factorized" (default via "auto"): exact fp64 O(N*M) two-pass
+    identity (row sums of G against S = sum_j u_j, column sums against
+    T = sum_i u_i / m_i); agrees with the reference to ~1e-15.
+    algorithm="gram": the symmetric N x N Gram on tcgen05 tensor cores
+    (3xTF32, fp32 TMEM blocks folded into an fp64 shadow) followed by the
+    row/column-sum epilogue — the reference's own formulation, within the
+    3xTF32 bound (1e-5 relative; K1).
     """
     t0 = time.perf_counter()
     resolve_workers(workers)
@@ -309,9 +311,7 @@ def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") 
         raise ValidationError(f"unknown pid algorithm {algorithm!r}; expected one of {PID_ALGORITHMS}")
     de = stage(ensemble)
     out = _Out(de.n, de.device)
-    use_gram = algorithm == "gram" or (
-        algorithm == "auto" and de.dtype_code == N.PIDB_F32 and _gram_available()
-    )
+    use_gram = algorithm == "gram"
     masses = _pid_gram(de, out) if use_gram else _pid_factorized(de, out)
     return _finish(de, out, "pid", masses, t0)
 
