@@ -333,10 +333,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   };
 
-  // ------------------------------------------------------ pipelined loop
+  // ------------------------------------------------------ tile loop
   int s_cur = 0;        // stage of tile j
   uint32_t par = 0;     // mbarrier parity of tile j
   int s_prev = 0;       // stage of tile j-1
+  if constexpr (ROWS == 0) {
+    // Large-N layouts: one resident tile, stages-1 tiles in flight (the
+    // memory latency, not the barrier count, is what limits these).
+    for (int64_t j = 0; j < my_tiles; ++j) {
+      mbar_wait(&full[s_cur], par);
+      unsigned char* st = tiles + (size_t)s_cur * p.stage_bytes;
+      if (mode != MODE_MASS) pass1(st, red);
+      __syncthreads();
+      finalize(j, 0);
+      __syncthreads();
+      pass2(st, 0);
+      __syncthreads();
+      if (tid == 0 && j + p.stages < my_tiles) issue(j + p.stages);
+      if (++s_cur == p.stages) { s_cur = 0; par ^= 1u; }
+    }
+  } else
   for (int64_t j = 0; j <= my_tiles; ++j) {
     const bool have = j < my_tiles;
     if (have) {
