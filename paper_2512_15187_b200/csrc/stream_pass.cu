@@ -85,6 +85,66 @@ __device__ __forceinline__ uint32_t swz_xor(uint32_t r) {
   else return (r >> 2) & 1u;
 }
 
+// CTA column partial -> global; the last CTA to finish reduces every CTA's
+// partials in a fixed order (grid, then column box) and resets the counter.
+// part layout: [grid][pncb * n][2] (row sums, masses); part_nb [grid][n].
+__device__ __forceinline__ void finish_partials(const StreamParams& p, int pncb, double col_acc,
+                                                unsigned* s_ticket, double* s_col) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = (int)p.n;
+  const int G = gridDim.x;
+  {
+    const double c = warp_sum(col_acc);
+    if (lane == 0) s_col[warp] = c;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int k = 0; k < kWarps; ++k) t += s_col[k];
+      p.part_col[blockIdx.x] = t;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) *s_ticket = atomicAdd(p.counter, 1u);
+  __syncthreads();
+  if (*s_ticket != (unsigned)(G - 1)) return;
+
+  __threadfence();
+  for (int r = warp; r < n; r += kWarps) {
+    double a = 0.0, b = 0.0;
+    int64_t nb = 0;
+    for (int g = lane; g < G; g += 32) {
+      for (int cb = 0; cb < pncb; ++cb) {
+        const double* src = p.part + ((size_t)g * pncb * n + cb * n + r) * 2;
+        a += __ldcg(src);
+        b += __ldcg(src + 1);
+      }
+      if (p.mode == MODE_MASS && p.part_nb != nullptr)
+        nb += (int64_t)__ldcg(reinterpret_cast<const long long*>(p.part_nb + (size_t)g * n + r));
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    if (lane == 0) {
+      if (p.mode == MODE_MASS) {
+        p.out_mass[r] = b;
+        if (p.out_nb) p.out_nb[r] = nb;
+      } else {
+        p.out_row[r] = a;
+        if (p.out_mass) p.out_mass[r] = b;
+      }
+    }
+  }
+  if (warp == 0 && p.mode == MODE_MEAN) {
+    double c = 0.0;
+    for (int g = lane; g < G; g += 32) c += __ldcg(p.part_col + g);
+    c = warp_sum(c);
+    if (lane == 0) p.out_col[0] = c;
+  }
+  if (tid == 0) *p.counter = 0u;  // ready for the next launch on this workspace
+}
+
 // ---------------------------------------------------------------------------
 // Kernel structure (software-pipelined over tiles, ONE block barrier per tile):
 //   iteration j:  wait TMA(tile j)
@@ -415,63 +475,267 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  {
-    const double c = warp_sum(col_acc);
-    if (lane == 0) s_col[warp] = c;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int k = 0; k < kWarps; ++k) t += s_col[k];
-      p.part_col[blockIdx.x] = t;
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) *s_ticket = atomicAdd(p.counter, 1u);
-  __syncthreads();
-  if (*s_ticket != (unsigned)(G - 1)) return;
-
-  // ------------------------------------------- last CTA: fixed-order reduce
-  __threadfence();
   constexpr int PNCB = ROWS > 0 ? 1 : NCB;
-  for (int r = warp; r < n; r += kWarps) {
-    double a = 0.0, b = 0.0;
-    int64_t nb = 0;
-    for (int g = lane; g < G; g += 32) {
-      for (int cb = 0; cb < PNCB; ++cb) {
-        const double* src = p.part + ((size_t)g * PNCB * n + cb * n + r) * 2;
-        a += __ldcg(src);
-        b += __ldcg(src + 1);
-      }
-      if (p.mode == MODE_MASS && p.part_nb != nullptr)
-        nb += (int64_t)__ldcg(reinterpret_cast<const long long*>(p.part_nb + (size_t)g * n + r));
-    }
-    a = warp_sum(a);
-    b = warp_sum(b);
+  finish_partials(p, PNCB, col_acc, s_ticket, s_col);
+}
+
+// ---------------------------------------------------------------------------
+// Large-N variant (n > 256): a tile is V = 2 x 128 B of cells (256 bytes per
+// member row, DRAM-friendly) for ALL members, streamed through SMEM in
+// 256-row chunks twice: touch 1 (column sweep) from HBM with an L2
+// evict_last hint, touch 2 (row sweep) re-reads the same chunks, served by
+// L2.  HBM traffic stays one read of the ensemble.  Thread t owns line
+// (column box t>>8, row t&255) of every chunk; its row sums for chunk c stay
+// in registers (acc[c], c < CMAX).
+constexpr int kChunkRows = 256;
+constexpr int kChunkBytes = 2 * kChunkRows * 128;  // 64 KB
+constexpr int kChunkBufs = 3;
+
+template <typename T, int CMAX>
+__global__ void __launch_bounds__(kThreads, 1)
+    chunked_pass_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
+  constexpr int EPC = Vec<T>::EPC;
+  constexpr int E = 128 / (int)sizeof(T);  // cells per 128-byte line
+  constexpr int V = 2 * E;                 // cells per tile
+  constexpr int P = kThreads / 16;         // row phases in touch 1 (16 chunk columns)
+  static_assert(kThreads == 2 * kChunkRows, "one (box, row) line per thread");
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  unsigned char* bufs = smem_raw + pad;
+  unsigned char* tail = bufs + (size_t)kChunkBufs * kChunkBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tail);
+  double* sS = reinterpret_cast<double*>(tail + 64);
+  double* sW = sS + V;
+  double* red = sW + V;  // [kWarps][V]
+  unsigned* s_ticket = reinterpret_cast<unsigned*>(red + kWarps * V);
+  double* s_col = reinterpret_cast<double*>(s_ticket + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = (int)p.n;
+  const int G = gridDim.x;
+  const int C = (n + kChunkRows - 1) / kChunkRows;
+  const int mode = p.mode;
+  const bool two_touch = mode != MODE_MASS;
+  const int loads_per_tile = two_touch ? 2 * C : C;
+  const bool weighted = p.w != nullptr;
+  const int64_t my_tiles = p.tiles > blockIdx.x ? (p.tiles - 1 - blockIdx.x) / G + 1 : 0;
+  const int64_t total_loads = my_tiles * loads_per_tile;
+  const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
+
+  if (tid == 0) {
+    prefetch_tma_desc(&tmap);
+    for (int b = 0; b < kChunkBufs; ++b) mbar_init(&full[b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int64_t q) {  // q-th chunk load of this CTA
+    const int b = (int)(q % kChunkBufs);
+    const int64_t j = q / loads_per_tile;
+    const int i = (int)(q - j * loads_per_tile);
+    const bool second = i >= C;
+    const int c = second ? i - C : i;
+    const int64_t tile = blockIdx.x + j * G;
+    unsigned char* dst = bufs + (size_t)b * kChunkBytes;
+    mbar_arrive_expect_tx(&full[b], kChunkBytes);
+    const uint64_t pol = (two_touch && !second) ? pol_keep : pol_drop;
+    for (int cb = 0; cb < 2; ++cb)
+      tma_load_2d(dst + cb * (kChunkRows * 128), &tmap, (int32_t)(tile * V + cb * E),
+                  c * kChunkRows, &full[b], pol);
+  };
+  if (tid == 0)
+    for (int64_t q = 0; q < total_loads && q < kChunkBufs; ++q) issue(q);
+
+  double acc_row[CMAX], acc_mass[CMAX];
+  int acc_nb[CMAX];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
-    if (lane == 0) {
-      if (p.mode == MODE_MASS) {
-        p.out_mass[r] = b;
-        if (p.out_nb) p.out_nb[r] = nb;
-      } else {
-        p.out_row[r] = a;
-        if (p.out_mass) p.out_mass[r] = b;
+  for (int c = 0; c < CMAX; ++c) { acc_row[c] = 0.0; acc_mass[c] = 0.0; acc_nb[c] = 0; }
+  double col_acc = 0.0;
+
+  // touch-1 coordinates: chunk column q16 (box, chunk), row phase ph
+  const int q16 = tid & 15, ph = tid >> 4;
+  const int a_cb = q16 >> 3, a_ch = q16 & 7;
+  const uint32_t a_off = (uint32_t)(a_cb * kChunkRows * 128 + ph * 128) +
+                         ((uint32_t)(a_ch ^ (ph & 7)) << 4);
+  // touch-2 coordinates: this thread's line
+  const int b_cb = tid >> 8, b_rr = tid & 255;
+  const uint32_t b_off = (uint32_t)(b_cb * kChunkRows * 128 + b_rr * 128);
+  const uint32_t b_xor = (uint32_t)(b_rr & 7);
+
+  int64_t q = 0;  // chunk loads consumed so far
+  auto next_chunk = [&]() -> const unsigned char* {
+    const int b = (int)(q % kChunkBufs);
+    mbar_wait(&full[b], (uint32_t)((q / kChunkBufs) & 1));
+    return bufs + (size_t)b * kChunkBytes;
+  };
+  auto release_chunk = [&]() {
+    __syncthreads();  // everyone is done with this buffer
+    if (tid == 0 && q + kChunkBufs < total_loads) issue(q + kChunkBufs);
+    ++q;
+  };
+
+  for (int64_t j = 0; j < my_tiles; ++j) {
+    const int64_t x0 = (blockIdx.x + j * G) * (int64_t)V;
+    // ---------------------------------------------------- touch 1 (columns)
+    if (two_touch) {
+      double part[EPC];
+      float2 sh01 = make_float2(1.0f, 1.0f), sh23 = sh01;
+      float2 sc01 = make_float2(0.0f, 0.0f), sc23 = sc01;
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) part[e] = 0.0;
+      for (int c = 0; c < C; ++c) {
+        const unsigned char* st = next_chunk();
+        const unsigned char* pa = st + a_off;
+        if constexpr (sizeof(T) == 4) {
+          if (mode == MODE_MEAN) {
+#pragma unroll
+            for (int k = 0; k < kChunkRows / P; ++k) {
+              const float4 v = Vec<float>::loadf(pa + k * (P * 128));
+              fast2sum_acc2(sh01, sc01, make_float2(v.x, v.y));
+              fast2sum_acc2(sh23, sc23, make_float2(v.z, v.w));
+            }
+          } else {
+#pragma unroll 4
+            for (int k = 0; k < kChunkRows / P; ++k) {
+              const int r = c * kChunkRows + ph + k * P;
+              double v[EPC];
+              Vec<T>::load(pa + k * (P * 128), v);
+              const double iv = r < n ? __ldg(p.inv + r) : 0.0;
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
+            }
+          }
+        } else {
+#pragma unroll 4
+          for (int k = 0; k < kChunkRows / P; ++k) {
+            const int r = c * kChunkRows + ph + k * P;
+            double v[EPC];
+            Vec<T>::load(pa + k * (P * 128), v);
+            const double iv = mode == MODE_MEAN ? 1.0 : (r < n ? __ldg(p.inv + r) : 0.0);
+#pragma unroll
+            for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
+          }
+        }
+        release_chunk();
+      }
+      if constexpr (sizeof(T) == 4) {
+        if (mode == MODE_MEAN) {
+          part[0] = ((double)sh01.x - 1.0) + (double)sc01.x;
+          part[1] = ((double)sh01.y - 1.0) + (double)sc01.y;
+          part[2] = ((double)sh23.x - 1.0) + (double)sc23.x;
+          part[3] = ((double)sh23.y - 1.0) + (double)sc23.y;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) part[e] += __shfl_xor_sync(0xffffffffu, part[e], 16);
+      if (lane < 16) {
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) red[warp * V + q16 * EPC + e] = part[e];
+      }
+    }
+    __syncthreads();
+    for (int v = tid; v < V; v += kThreads) {
+      const int64_t x = x0 + v;
+      const double wx = x < p.m ? (weighted ? __ldg(p.w + x) : 1.0) : 0.0;
+      sW[v] = wx;
+      if (two_touch) {
+        double S = 0.0;
+#pragma unroll
+        for (int k = 0; k < kWarps; ++k) S += red[k * V + v];
+        sS[v] = wx * S;
+        col_acc = fma(wx, S, col_acc);
+      }
+    }
+    __syncthreads();
+    // ------------------------------------------------------- touch 2 (rows)
+    const double* S = sS + b_cb * E;
+    const double* W = sW + b_cb * E;
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c) {
+      if (c < C) {
+        const unsigned char* line = next_chunk() + b_off;
+        if (c * kChunkRows + b_rr < n) {
+          double ar[EPC], am[EPC];
+          int nb = 0;
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) { ar[e] = 0.0; am[e] = 0.0; }
+#pragma unroll
+          for (int L = 0; L < 8; ++L) {
+            double v[EPC];
+            Vec<T>::load(line + ((L ^ b_xor) << 4), v);
+            const int vb = L * EPC;
+            if (mode == MODE_MASS) {
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) {
+                am[e] = fma(v[e], W[vb + e], am[e]);
+                nb += is_nonbinary(v[e]);
+              }
+            } else if (mode == MODE_COLS) {
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) ar[e] = fma(v[e], S[vb + e], ar[e]);
+            } else if (weighted) {
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) {
+                ar[e] = fma(v[e], S[vb + e], ar[e]);
+                am[e] = fma(v[e], W[vb + e], am[e]);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) {
+                ar[e] = fma(v[e], S[vb + e], ar[e]);
+                am[e] += v[e];
+              }
+            }
+          }
+          double tr = ar[0], tm = am[0];
+#pragma unroll
+          for (int e = 1; e < EPC; ++e) { tr += ar[e]; tm += am[e]; }
+          acc_row[c] += tr;
+          acc_mass[c] += tm;
+          acc_nb[c] += nb;
+        }
+        release_chunk();
       }
     }
   }
-  if (warp == 0 && p.mode == MODE_MEAN) {
-    double c = 0.0;
-    for (int g = lane; g < G; g += 32) c += __ldcg(p.part_col + g);
-    c = warp_sum(c);
-    if (lane == 0) p.out_col[0] = c;
+
+  // ------------------------------------------------ CTA partials -> global
+#pragma unroll
+  for (int c = 0; c < CMAX; ++c) {
+    const int r = c * kChunkRows + b_rr;
+    if (c < C && r < n) {
+      double* dst = p.part + ((size_t)blockIdx.x * 2 * n + b_cb * n + r) * 2;
+      dst[0] = acc_row[c];
+      dst[1] = acc_mass[c];
+    }
   }
-  if (tid == 0) *p.counter = 0u;  // ready for the next launch on this workspace
+  if (p.mode == MODE_MASS && p.part_nb != nullptr) {
+    int64_t* nbp = p.part_nb + (size_t)blockIdx.x * n;
+    if (b_cb == 0) {
+#pragma unroll
+      for (int c = 0; c < CMAX; ++c) {
+        const int r = c * kChunkRows + b_rr;
+        if (c < C && r < n) nbp[r] = acc_nb[c];
+      }
+    }
+    __syncthreads();
+    if (b_cb == 1) {
+#pragma unroll
+      for (int c = 0; c < CMAX; ++c) {
+        const int r = c * kChunkRows + b_rr;
+        if (c < C && r < n)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&nbp[r]), (unsigned long long)acc_nb[c]);
+      }
+    }
+  }
+  finish_partials(p, 2, col_acc, s_ticket, s_col);
 }
 
 // ---------------------------------------------------------------- host side
 struct Plan {
   int lb, ncb, ipt, rows, boxr, nrb, stages, grid;
+  bool chunked;
   uint32_t stage_bytes;
   size_t smem;
   int64_t tiles;
@@ -481,8 +745,27 @@ constexpr size_t kSmemBudget = 227 * 1024;
 
 size_t tail_bytes(int V) { return 64 + (size_t)V * 8 * 4 + (size_t)2 * kWarps * V * 8 + 16 + kWarps * 8 + 64; }
 
+constexpr int kChunkMax = 16;  // chunked layout: n <= 4096
+bool use_chunked(int64_t n) { return n > 256 && n <= (int64_t)kChunkMax * kChunkRows; }
+size_t chunked_smem() {
+  return 1024 + (size_t)kChunkBufs * kChunkBytes + 64 + (size_t)(2 + kWarps) * 64 * 8 + 16 +
+         kWarps * 8 + 64;
+}
+
 bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
   if (n < 1 || m < 1) return false;
+  pl.chunked = false;
+  if (use_chunked(n)) {  // wide tiles, two touches through L2 (see chunked_pass_kernel)
+    const int V = 2 * 128 / esize;
+    pl.chunked = true;
+    pl.lb = 128; pl.ncb = 2; pl.ipt = 1; pl.rows = 0;
+    pl.boxr = kChunkRows; pl.nrb = (int)((n + kChunkRows - 1) / kChunkRows);
+    pl.stages = kChunkBufs; pl.stage_bytes = kChunkBytes;
+    pl.smem = chunked_smem();
+    pl.tiles = (m + V - 1) / V;
+    pl.grid = (int)std::min<int64_t>(pl.tiles, sm_count());
+    return true;
+  }
   const int nrb = (int)((n + 255) / 256);
   const int boxr_full = (int)(((n + nrb - 1) / nrb + 7) / 8 * 8);
   const int rows = nrb * boxr_full;
@@ -565,6 +848,24 @@ int launch_layout(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaS
   return launch_ipt<T, 32, 1>(tm, sp, pl, st);
 }
 
+template <typename T, int CMAX>
+int launch_chunked_t(const CUtensorMap& tm, StreamParams& sp, int grid, cudaStream_t st) {
+  auto kern = chunked_pass_kernel<T, CMAX>;
+  const size_t smem = chunked_smem();
+  PIDB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, kThreads, smem, st>>>(tm, sp);
+  PIDB_LAUNCH_CHECK("chunked_pass_kernel");
+  return PIDB_OK;
+}
+
+template <typename T>
+int launch_chunked(const CUtensorMap& tm, StreamParams& sp, int grid, cudaStream_t st) {
+  const int C = (int)((sp.n + kChunkRows - 1) / kChunkRows);
+  if (C <= 4) return launch_chunked_t<T, 4>(tm, sp, grid, st);
+  if (C <= 8) return launch_chunked_t<T, 8>(tm, sp, grid, st);
+  return launch_chunked_t<T, 16>(tm, sp, grid, st);
+}
+
 int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
                     const double* w, const double* inv, double* out_row, double* out_mass,
                     double* out_col, int64_t* out_nb, void* ws, size_t ws_bytes, void* stream) {
@@ -612,6 +913,9 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
   base += align_up((size_t)pl.grid * n * sizeof(int64_t), 256);
   sp.out_row = out_row; sp.out_mass = out_mass; sp.out_col = out_col; sp.out_nb = out_nb;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (pl.chunked)
+    return dtype == PIDB_F32 ? launch_chunked<float>(tm, sp, pl.grid, st)
+                             : launch_chunked<double>(tm, sp, pl.grid, st);
   return dtype == PIDB_F32 ? launch_layout<float>(tm, sp, pl, st)
                            : launch_layout<double>(tm, sp, pl, st);
 }
