@@ -114,6 +114,20 @@ __device__ __forceinline__ void fast2sum_acc(float& s, float& c, float x) {
   s = t;
 }
 
+// 16-byte async global->shared copy (LDGSTS, L1 bypass); src_bytes < 16
+// zero-fills the tail of the chunk.
+__device__ __forceinline__ void cp_async16(uint32_t smem_dst, const void* src, uint32_t src_bytes,
+                                           uint64_t policy) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(smem_dst),
+               "l"(src), "r"(src_bytes), "l"(policy)
+               : "memory");
+}
+// Arrive on `bar` once every cp.async this thread issued so far has landed.
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
 // Packed fp32x2 arithmetic (sm_100 FADD2): two lanes of work per instruction.
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   float2 r;

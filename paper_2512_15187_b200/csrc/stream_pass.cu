@@ -1,4 +1,5 @@
-// K5 (PID-mean partials, one HBM pass) and K9-B (exact-PID column sums).
+// K5 (PID-mean partials, one HBM pass), K9-B (exact-PID column sums) and K6
+// (member masses + non-binary counts): the streaming kernels of the depth path.
 //
 // Reference path replaced:
 //   depth_pid_mean          /root/reference/pkg/src/fuzzdepth/depth.py:246-287
@@ -6,50 +7,59 @@
 //     mask_mass(mean)       /root/reference/pkg/src/fuzzdepth/grid.py:242-244
 //     _member_mean_terms    /root/reference/pkg/src/fuzzdepth/depth.py:231-243
 //   _pairwise_sums col_inv  /root/reference/pkg/src/fuzzdepth/depth.py:157,160 (K9-B)
+//   member_masses           /root/reference/pkg/src/fuzzdepth/depth.py:88-102 (K6)
 //
-// Layout: members are rows of a (n x m) row-major matrix in HBM.  A "tile" is
-// V consecutive cells of ALL n members; one 2D TMA box per (column box, row
-// box) brings it to shared memory with a 128/64/32-byte swizzle, so the same
-// bytes are read from HBM exactly once and consumed twice from SMEM:
+// Layout: members are rows of an (n x m) row-major matrix in HBM.  A "tile"
+// is the next 256 bytes of cells (V = 64 fp32 / 32 fp64) of EVERY member,
+// fetched by one 2D TMA box (256-byte rows, no swizzle: TMA streams reach
+// ~6.7 TB/s with 256-byte rows but stall at ~4.6 TB/s with 128-byte rows,
+// tools/ubench_tma.cu), so HBM is read exactly once and the tile is consumed
+// twice from SMEM:
 //   pass 1 (column sweep): S(x) = sum_i u_i(x)        [MODE_MEAN]
 //                           T(x) = sum_i inv_i u_i(x)  [MODE_COLS]
 //   pass 2 (row sweep)   : acc_i += u_i(x) * w(x) S(x),  mass_i += w(x) u_i(x)
-// Pass 1 for fp32 data uses an error-free Fast2Sum in fp32 (seeded with 1.0 so
-// that |s| >= |u| always holds; values are in [0,1]) and pass 2 converts each
-// value once to fp64 (DFMA/DADD accumulation).  Each thread owns fixed
-// (column box, member) items for the whole persistent CTA lifetime, so the
-// member partials live in registers; CTA partials are reduced by the last CTA
-// in a fixed order (bit-reproducible on a given device).
+// Pass 1 on fp32 data is an error-free Fast2Sum in packed fp32 (FADD2, seeded
+// with 1.0 so |s| >= |u| holds for mask values in [0,1]), combined in fp64;
+// pass 2 converts each value once to fp64 (DFMA/DADD).  CTA partials are
+// reduced by the last CTA in a fixed order (bit-reproducible per device).
+//
+// Two kernels:
+//   rows_kernel    (n <= 256): software-pipelined tiles (pass 1 of tile j
+//                  overlaps pass 2 of tile j-1, one barrier per tile); warp w
+//                  owns rows w, w+16, ..., lane l owns 8 bytes of each row, the
+//                  row sums stay in registers for the whole kernel.
+//   chunked_kernel (256 < n <= 4096): the tile is streamed in 256-row chunks
+//                  twice; touch 1 (columns) comes from HBM with an L2
+//                  evict_last hint, touch 2 (rows) re-reads the chunks from L2.
 #include "common.cuh"
 
 namespace pidb {
 namespace {
 
-#ifndef PIDB_K5_THREADS
-#define PIDB_K5_THREADS 512
-#endif
-constexpr int kThreads = PIDB_K5_THREADS;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
+constexpr int kRowBytes = 256;          // bytes of one member row per tile
+constexpr int kChunks16 = kRowBytes / 16;
+constexpr int kPhases = kThreads / kChunks16;  // row phases of the column sweep
 constexpr int MODE_MEAN = 0;
 constexpr int MODE_COLS = 1;
-constexpr int MODE_MASS = 2;  // masses (+ nonbinary count) only: pass 2 without pass 1
+constexpr int MODE_MASS = 2;  // masses (+ non-binary count): row sweep only
 
 struct StreamParams {
   int64_t n, m, tiles;
-  int nrb, boxr;          // row boxes per column box, rows per box (multiple of 8)
   int stages;
-  uint32_t stage_bytes;   // bytes of one tile in smem
+  uint32_t stage_bytes;  // bytes of one tile (rows kernel) or chunk (chunked)
   int mode;
-  const double* w;        // nullable
-  const double* inv;      // MODE_COLS
-  double* part;           // [grid][items][2]
-  double* part_col;       // [grid]
-  int64_t* part_nb;       // [grid][n] (MODE_MASS, nullable)
+  const double* w;       // nullable
+  const double* inv;     // MODE_COLS
+  double* part;          // [grid][pncb * n][2]
+  double* part_col;      // [grid]
+  int64_t* part_nb;      // [grid][n] (MODE_MASS, nullable)
   unsigned* counter;
-  double* out_row;        // n
-  double* out_mass;       // n (nullable in MODE_COLS)
-  double* out_col;        // 1 (MODE_MEAN)
-  int64_t* out_nb;        // n (MODE_MASS, nullable)
+  double* out_row;       // n
+  double* out_mass;      // n (nullable in MODE_COLS)
+  double* out_col;       // 1 (MODE_MEAN)
+  int64_t* out_nb;       // n (MODE_MASS, nullable)
 };
 
 template <typename T>
@@ -76,18 +86,61 @@ struct Vec<double> {
 
 __device__ __forceinline__ bool is_nonbinary(double x) { return !(x == 0.0 || x == 1.0); }
 
-// XOR applied to the 16-byte chunk index of line `r` by the TMA swizzle
-// (rows of one column box are consecutive lines, boxes are 8-line aligned).
-template <int LB>
-__device__ __forceinline__ uint32_t swz_xor(uint32_t r) {
-  if constexpr (LB == 128) return r & 7u;
-  else if constexpr (LB == 64) return (r >> 1) & 3u;
-  else return (r >> 2) & 1u;
-}
+// Column sweep over 256-byte rows: this thread's 16-byte chunk of rows
+// r0, r0 + kPhases, ... < r_end, starting at `pa`.  fp32 MODE_MEAN uses the
+// Fast2Sum state; otherwise part[] += iv(row) * u in fp64.
+template <typename T>
+struct ColSweep {
+  static constexpr int EPC = Vec<T>::EPC;
+  float2 sh01, sh23, sc01, sc23;
+  double part[EPC];
+  __device__ void reset() {
+    sh01 = sh23 = make_float2(1.0f, 1.0f);
+    sc01 = sc23 = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) part[e] = 0.0;
+  }
+  // rg: global member index of row r0 (for inv); rows >= n contribute 0
+  __device__ void run(const unsigned char* pa, int r0, int r_end, int mode, const double* inv,
+                      int rg, int n) {
+    if constexpr (sizeof(T) == 4) {
+      if (mode == MODE_MEAN) {
+#pragma unroll 4
+        for (int r = r0; r < r_end; r += kPhases, pa += kPhases * kRowBytes) {
+          const float4 v = Vec<float>::loadf(pa);
+          fast2sum_acc2(sh01, sc01, make_float2(v.x, v.y));
+          fast2sum_acc2(sh23, sc23, make_float2(v.z, v.w));
+        }
+        return;
+      }
+    }
+#pragma unroll 4
+    for (int r = r0; r < r_end; r += kPhases, rg += kPhases, pa += kPhases * kRowBytes) {
+      double v[EPC];
+      Vec<T>::load(pa, v);
+      const double iv = mode == MODE_MEAN ? 1.0 : (rg < n ? __ldg(inv + rg) : 0.0);
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
+    }
+  }
+  // fold the Fast2Sum state into part[] and combine the warp's two row
+  // phases (lanes l and l^16 share a chunk); lanes < 16 hold the result
+  __device__ void combine(int mode) {
+    if constexpr (sizeof(T) == 4) {
+      if (mode == MODE_MEAN) {
+        part[0] = ((double)sh01.x - 1.0) + (double)sc01.x;
+        part[1] = ((double)sh01.y - 1.0) + (double)sc01.y;
+        part[2] = ((double)sh23.x - 1.0) + (double)sc23.x;
+        part[3] = ((double)sh23.y - 1.0) + (double)sc23.y;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) part[e] += __shfl_xor_sync(0xffffffffu, part[e], 16);
+  }
+};
 
 // CTA column partial -> global; the last CTA to finish reduces every CTA's
-// partials in a fixed order (grid, then column box) and resets the counter.
-// part layout: [grid][pncb * n][2] (row sums, masses); part_nb [grid][n].
+// partials in a fixed order (grid, then half) and resets the counter.
 __device__ __forceinline__ void finish_partials(const StreamParams& p, int pncb, double col_acc,
                                                 unsigned* s_ticket, double* s_col) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -145,56 +198,50 @@ __device__ __forceinline__ void finish_partials(const StreamParams& p, int pncb,
   if (tid == 0) *p.counter = 0u;  // ready for the next launch on this workspace
 }
 
+// sS/sW for tile cells [x0, x0+V): w*S (or w*T) and w; col_acc += w*S.
+template <int V>
+__device__ __forceinline__ void finalize_tile(const StreamParams& p, const double* rd, int64_t x0,
+                                              double* sS, double* sW, bool colsum,
+                                              double& col_acc) {
+  for (int v = threadIdx.x; v < V; v += kThreads) {
+    const int64_t x = x0 + v;
+    const double wx = x < p.m ? (p.w ? __ldg(p.w + x) : 1.0) : 0.0;
+    sW[v] = wx;
+    if (colsum) {
+      double S = 0.0;
+#pragma unroll
+      for (int k = 0; k < kWarps; ++k) S += rd[k * V + v];
+      sS[v] = wx * S;
+      col_acc = fma(wx, S, col_acc);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
-// Kernel structure (software-pipelined over tiles, ONE block barrier per tile):
-//   iteration j:  wait TMA(tile j)
-//                 pass 1(tile j): column partials -> red[]          (all threads)
-//                 __syncthreads
-//                 refill: TMA(tile j-2+stages) into the stage tile j-2 used
-//                 finalize(tile j): S, w*S, w -> sS/sW[j&1]          (V threads)
-//                 pass 2(tile j-1): row sums against sS/sW[(j-1)&1]  (all threads)
-// so finalize and pass 2 overlap other warps' work instead of serialising
-// behind two barriers.  Pass 2 has two register layouts:
-//   ROWS>0 : (128-byte lines, 2 column boxes) lane l owns 8 bytes of the row's
-//            64-cell tile slice (lanes 0-15 box 0, 16-31 box 1), warp w owns
-//            rows w, w+W, ..., accumulators stay in registers for the whole
-//            kernel and are reduced across lanes once at the end;
-//   ROWS==0: thread owns (column box, member) items (large N), IPT per thread.
-template <typename T, int LB, int NCB, int IPT, int ROWS>
+// rows_kernel: n <= 256, ROWS = ceil(n / 16) rows per warp.
+template <typename T, int ROWS>
 __global__ void __launch_bounds__(kThreads, 1)
-    stream_pass_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
-  constexpr int EPC = Vec<T>::EPC;              // elements per 16-byte chunk
-  constexpr int E = LB / (int)sizeof(T);        // elements per line (box inner)
-  constexpr int V = NCB * E;                    // cells per tile
-  constexpr int CPL = LB / 16;                  // chunks per line
-  constexpr int QC = NCB * CPL;                 // chunks per tile row
-  constexpr int P = kThreads / QC;              // row phases in pass 1
-  constexpr int EPL = 8 / (int)sizeof(T);       // elements per lane in ROWS pass 2
-  static_assert(kThreads % QC == 0 && QC <= 32 && P % 8 == 0 && kWarps % 8 == 0, "layout");
-  static_assert(ROWS == 0 || (LB == 128 && NCB == 2), "row-resident pass 2 needs 2x128B lines");
+    rows_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
+  constexpr int EPC = Vec<T>::EPC;
+  constexpr int V = kRowBytes / (int)sizeof(T);  // cells per tile
+  constexpr int EPL = 8 / (int)sizeof(T);        // elements per lane in pass 2
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // dynamic smem base rounded up to 1024 B (swizzle atom) without leaving the
-  // shared address space (keeps LDS instead of generic loads)
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   unsigned char* tiles = smem_raw + pad;
   unsigned char* tail = tiles + (size_t)p.stages * p.stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(tail);
-  double* sS = reinterpret_cast<double*>(tail + 64);     // [2][V]: w*S (or w*T)
-  double* sW = sS + 2 * V;                                 // [2][V]: w
-  double* red = sW + 2 * V;                                // [2][kWarps][V]
+  double* sS = reinterpret_cast<double*>(tail + 128);  // [2][V]
+  double* sW = sS + 2 * V;                              // [2][V]
+  double* red = sW + 2 * V;                             // [2][kWarps][V]
   unsigned* s_ticket = reinterpret_cast<unsigned*>(red + 2 * kWarps * V);
   double* s_col = reinterpret_cast<double*>(s_ticket + 2);
 
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = (int)p.n;
   const int G = gridDim.x;
-  const bool weighted = p.w != nullptr;
   const int mode = p.mode;
-  const int items = NCB * n;
-  const int cb_rows = p.nrb * p.boxr;  // lines per column box
-
+  const bool weighted = p.w != nullptr;
   const int64_t my_tiles = p.tiles > blockIdx.x ? (p.tiles - 1 - blockIdx.x) / G + 1 : 0;
   const uint64_t pol = policy_evict_first();
 
@@ -205,300 +252,125 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
 
-  auto issue = [&](int64_t j) {  // local tile j -> stage j % stages
+  auto issue = [&](int64_t j) {  // local tile j -> stage j % stages (thread 0)
     const int s = (int)(j % p.stages);
-    const int64_t tile = blockIdx.x + j * G;
-    unsigned char* dst = tiles + (size_t)s * p.stage_bytes;
-    mbar_arrive_expect_tx(&full[s], p.stage_bytes);
-    for (int cb = 0; cb < NCB; ++cb)
-      for (int rb = 0; rb < p.nrb; ++rb)
-        tma_load_2d(dst + (size_t)(cb * p.nrb + rb) * p.boxr * LB, &tmap,
-                    (int32_t)(tile * V + cb * E), rb * p.boxr, &full[s], pol);
+    mbar_arrive_expect_tx(&full[s], (uint32_t)n * kRowBytes);
+    tma_load_2d(tiles + (size_t)s * p.stage_bytes, &tmap, (int32_t)((blockIdx.x + j * G) * V), 0,
+                &full[s], pol);
   };
   if (tid == 0)
     for (int64_t j = 0; j < my_tiles && j < p.stages; ++j) issue(j);
 
-  // ------------------------------------------------------ pass-2 state
-  constexpr int NACC = ROWS > 0 ? ROWS : IPT;
-  double acc_row[NACC], acc_mass[NACC];
-  int acc_nb[NACC];
+  double acc_row[ROWS], acc_mass[ROWS];
+  int acc_nb[ROWS];
 #pragma unroll
-  for (int k = 0; k < NACC; ++k) { acc_row[k] = 0.0; acc_mass[k] = 0.0; acc_nb[k] = 0; }
-  // ROWS layout: lane -> (column box, 8-byte slot) of every owned row
-  const int r_cb = lane >> 4, r_pos = lane & 15;
-  const int r_cell = r_cb * E + r_pos * EPL;  // first tile cell of this lane
-  // ITEMS layout: item = cb*n + r, fixed per thread
-  uint32_t it_line[ROWS > 0 ? 1 : IPT];
-  uint32_t it_xor[ROWS > 0 ? 1 : IPT];
-  int it_vb[ROWS > 0 ? 1 : IPT];
-  if constexpr (ROWS == 0) {
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      const int it = tid + k * kThreads;
-      const int cb = it < items ? it / n : 0;
-      const int r = it < items ? it - cb * n : 0;
-      it_line[k] = (uint32_t)((cb * cb_rows + r) * LB);
-      it_xor[k] = swz_xor<LB>((uint32_t)r);
-      it_vb[k] = cb * E;
-    }
-  }
+  for (int k = 0; k < ROWS; ++k) { acc_row[k] = 0.0; acc_mass[k] = 0.0; acc_nb[k] = 0; }
   double col_acc = 0.0;
 
-  // pass-1 coordinates: chunk column q (cb, ch), row phase ph; the swizzle
-  // XOR of rows ph, ph+P, ... is constant because P is a multiple of 8.
-  const int q = tid % QC, ph = tid / QC;
-  const int q_cb = q / CPL, q_ch = q % CPL;
-  const uint32_t p1_off = (uint32_t)((q_cb * cb_rows + ph) * LB) +
-                          ((q_ch ^ swz_xor<LB>((uint32_t)ph)) << 4);
-
-  // ------------------------------------------------------ the two passes
-  auto pass1 = [&](const unsigned char* st, double* red) {
-    double part[EPC];
-    const unsigned char* pa = st + p1_off;
-    if constexpr (sizeof(T) == 4) {
-      if (mode == MODE_MEAN) {
-        float2 sh01 = make_float2(1.0f, 1.0f), sh23 = sh01;
-        float2 sc01 = make_float2(0.0f, 0.0f), sc23 = sc01;
-#pragma unroll 4
-        for (int r = ph; r < n; r += P, pa += P * LB) {
-          const float4 v = Vec<float>::loadf(pa);
-          fast2sum_acc2(sh01, sc01, make_float2(v.x, v.y));
-          fast2sum_acc2(sh23, sc23, make_float2(v.z, v.w));
-        }
-        part[0] = ((double)sh01.x - 1.0) + (double)sc01.x;
-        part[1] = ((double)sh01.y - 1.0) + (double)sc01.y;
-        part[2] = ((double)sh23.x - 1.0) + (double)sc23.x;
-        part[3] = ((double)sh23.y - 1.0) + (double)sc23.y;
-      } else {
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) part[e] = 0.0;
-#pragma unroll 4
-        for (int r = ph; r < n; r += P, pa += P * LB) {
-          double v[EPC];
-          Vec<T>::load(pa, v);
-          const double iv = __ldg(p.inv + r);
-#pragma unroll
-          for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < EPC; ++e) part[e] = 0.0;
-#pragma unroll 4
-      for (int r = ph; r < n; r += P, pa += P * LB) {
-        double v[EPC];
-        Vec<T>::load(pa, v);
-        const double iv = mode == MODE_MEAN ? 1.0 : __ldg(p.inv + r);
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
-      }
-    }
-    // combine the row phases inside this warp (lanes sharing q), fixed order
-#pragma unroll
-    for (int o = QC; o < 32; o <<= 1)
-#pragma unroll
-      for (int e = 0; e < EPC; ++e) part[e] += __shfl_xor_sync(0xffffffffu, part[e], o);
-    if (lane < QC) {
-#pragma unroll
-      for (int e = 0; e < EPC; ++e) red[warp * V + q * EPC + e] = part[e];
-    }
-  };
-
-  auto finalize = [&](int64_t j, int buf) {  // threads < V
-    const double* rd = red + buf * kWarps * V;
-    const int64_t x0 = (blockIdx.x + j * G) * (int64_t)V;
-    for (int v = tid; v < V; v += kThreads) {
-      const int64_t x = x0 + v;
-      const double wx = x < p.m ? (weighted ? __ldg(p.w + x) : 1.0) : 0.0;
-      sW[buf * V + v] = wx;
-      if (mode != MODE_MASS) {
-        double S = 0.0;
-#pragma unroll
-        for (int k = 0; k < kWarps; ++k) S += rd[k * V + v];
-        sS[buf * V + v] = wx * S;
-        col_acc = fma(wx, S, col_acc);
-      }
-    }
-  };
+  const int q = tid & (kChunks16 - 1), ph = tid / kChunks16;
+  const uint32_t p1_off = (uint32_t)(ph * kRowBytes + q * 16);
+  const uint32_t p2_off = (uint32_t)(warp * kRowBytes + lane * 8);
+  const int cell = lane * EPL;
 
   auto pass2 = [&](const unsigned char* st, int buf) {
-    const double* S = sS + buf * V;
-    const double* W = sW + buf * V;
-    if constexpr (ROWS > 0) {
-      double s_l[EPL], w_l[EPL];
+    double s_l[EPL], w_l[EPL];
 #pragma unroll
-      for (int e = 0; e < EPL; ++e) { s_l[e] = S[r_cell + e]; w_l[e] = W[r_cell + e]; }
-      // rows warp, warp+kWarps, ... share r & 7, hence one swizzled lane offset
-      const unsigned char* lane_base = st + (uint32_t)((r_cb * cb_rows + warp) * LB) +
-                                       ((uint32_t)((r_pos >> 1) ^ (warp & 7)) << 4) +
-                                       (uint32_t)((r_pos & 1) * 8);
-#define PIDB_ROWS_LOOP(BODY)                                                          \
-  _Pragma("unroll") for (int k = 0; k < ROWS; ++k) {                                  \
-    if (k < ROWS - 1 || warp + k * kWarps < n) {                                      \
-      const unsigned char* a = lane_base + k * (kWarps * LB);                         \
-      double v[EPL];                                                                  \
-      if constexpr (sizeof(T) == 4) {                                                 \
-        const float2 f = *reinterpret_cast<const float2*>(a);                        \
-        v[0] = f.x; v[EPL - 1] = f.y;                                                 \
-      } else {                                                                        \
-        v[0] = *reinterpret_cast<const double*>(a);                                   \
-      }                                                                               \
-      _Pragma("unroll") for (int e = 0; e < EPL; ++e) { BODY; }                       \
-    }                                                                                 \
-  }
-      if (mode == MODE_MEAN && !weighted) {
-        PIDB_ROWS_LOOP(acc_row[k] = fma(v[e], s_l[e], acc_row[k]); acc_mass[k] += v[e])
-      } else if (mode == MODE_MASS) {
-        PIDB_ROWS_LOOP(acc_mass[k] = fma(v[e], w_l[e], acc_mass[k]); acc_nb[k] += is_nonbinary(v[e]))
-      } else if (mode == MODE_COLS) {
-        PIDB_ROWS_LOOP(acc_row[k] = fma(v[e], s_l[e], acc_row[k]))
-      } else {
-        PIDB_ROWS_LOOP(acc_row[k] = fma(v[e], s_l[e], acc_row[k]);
-                       acc_mass[k] = fma(v[e], w_l[e], acc_mass[k]))
-      }
-#undef PIDB_ROWS_LOOP
-    } else {
-#define PIDB_ITEMS_LOOP(BODY)                                                         \
-  _Pragma("unroll") for (int k = 0; k < IPT; ++k) {                                   \
-    if (tid + k * kThreads < items) {                                                 \
-      const unsigned char* line = st + it_line[k];                                    \
-      const double* Sk = S + it_vb[k];                                                \
-      const double* Wk = W + it_vb[k];                                                \
-      double ar[EPC], am[EPC];                                                        \
-      int nb = 0;                                                                     \
-      _Pragma("unroll") for (int e = 0; e < EPC; ++e) { ar[e] = 0.0; am[e] = 0.0; }   \
-      _Pragma("unroll") for (int L = 0; L < CPL; ++L) {                               \
-        double v[EPC];                                                                \
-        Vec<T>::load(line + ((L ^ it_xor[k]) << 4), v);                               \
-        const int vb = L * EPC;                                                       \
-        _Pragma("unroll") for (int e = 0; e < EPC; ++e) { BODY; }                     \
-      }                                                                               \
-      double tr = ar[0], tm = am[0];                                                  \
-      _Pragma("unroll") for (int e = 1; e < EPC; ++e) { tr += ar[e]; tm += am[e]; }   \
-      acc_row[k] += tr;                                                               \
-      acc_mass[k] += tm;                                                              \
-      acc_nb[k] += nb;                                                                \
-    }                                                                                 \
-  }
-      if (mode == MODE_MEAN && !weighted) {
-        PIDB_ITEMS_LOOP(ar[e] = fma(v[e], Sk[vb + e], ar[e]); am[e] += v[e])
-      } else if (mode == MODE_MASS) {
-        PIDB_ITEMS_LOOP(am[e] = fma(v[e], Wk[vb + e], am[e]); nb += is_nonbinary(v[e]))
-      } else if (mode == MODE_COLS) {
-        PIDB_ITEMS_LOOP(ar[e] = fma(v[e], Sk[vb + e], ar[e]))
-      } else {
-        PIDB_ITEMS_LOOP(ar[e] = fma(v[e], Sk[vb + e], ar[e]); am[e] = fma(v[e], Wk[vb + e], am[e]))
-      }
-#undef PIDB_ITEMS_LOOP
+    for (int e = 0; e < EPL; ++e) {
+      s_l[e] = sS[buf * V + cell + e];
+      w_l[e] = sW[buf * V + cell + e];
     }
+    const unsigned char* base = st + p2_off;
+#define PIDB_ROWS_LOOP(BODY)                                                \
+  _Pragma("unroll") for (int k = 0; k < ROWS; ++k) {                        \
+    if (k < ROWS - 1 || warp + k * kWarps < n) {                            \
+      const unsigned char* a = base + k * (kWarps * kRowBytes);             \
+      double v[EPL];                                                        \
+      if constexpr (sizeof(T) == 4) {                                       \
+        const float2 f = *reinterpret_cast<const float2*>(a);              \
+        v[0] = f.x; v[EPL - 1] = f.y;                                       \
+      } else {                                                              \
+        v[0] = *reinterpret_cast<const double*>(a);                         \
+      }                                                                     \
+      _Pragma("unroll") for (int e = 0; e < EPL; ++e) { BODY; }             \
+    }                                                                       \
+  }
+    if (mode == MODE_MEAN && !weighted) {
+      PIDB_ROWS_LOOP(acc_row[k] = fma(v[e], s_l[e], acc_row[k]); acc_mass[k] += v[e])
+    } else if (mode == MODE_MASS) {
+      PIDB_ROWS_LOOP(acc_mass[k] = fma(v[e], w_l[e], acc_mass[k]); acc_nb[k] += is_nonbinary(v[e]))
+    } else if (mode == MODE_COLS) {
+      PIDB_ROWS_LOOP(acc_row[k] = fma(v[e], s_l[e], acc_row[k]))
+    } else {
+      PIDB_ROWS_LOOP(acc_row[k] = fma(v[e], s_l[e], acc_row[k]);
+                     acc_mass[k] = fma(v[e], w_l[e], acc_mass[k]))
+    }
+#undef PIDB_ROWS_LOOP
   };
 
-  // ------------------------------------------------------ tile loop
-  int s_cur = 0;        // stage of tile j
-  uint32_t par = 0;     // mbarrier parity of tile j
-  int s_prev = 0;       // stage of tile j-1
-  if constexpr (ROWS == 0) {
-    // Large-N layouts: one resident tile, stages-1 tiles in flight (the
-    // memory latency, not the barrier count, is what limits these).
-    for (int64_t j = 0; j < my_tiles; ++j) {
-      mbar_wait(&full[s_cur], par);
-      unsigned char* st = tiles + (size_t)s_cur * p.stage_bytes;
-      if (mode != MODE_MASS) pass1(st, red);
-      __syncthreads();
-      finalize(j, 0);
-      __syncthreads();
-      pass2(st, 0);
-      __syncthreads();
-      if (tid == 0 && j + p.stages < my_tiles) issue(j + p.stages);
-      if (++s_cur == p.stages) { s_cur = 0; par ^= 1u; }
-    }
-  } else
+  ColSweep<T> cs;
+  int s_cur = 0, s_prev = 0;
+  uint32_t par = 0;
   for (int64_t j = 0; j <= my_tiles; ++j) {
     const bool have = j < my_tiles;
+    double* rd = red + (j & 1) * kWarps * V;
     if (have) {
       mbar_wait(&full[s_cur], par);
-      if (mode != MODE_MASS)
-        pass1(tiles + (size_t)s_cur * p.stage_bytes, red + (j & 1) * kWarps * V);
+      if (mode != MODE_MASS) {
+        cs.reset();
+        cs.run(tiles + (size_t)s_cur * p.stage_bytes + p1_off, ph, n, mode, p.inv, ph, n);
+        cs.combine(mode);
+        if (lane < 16) {
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) rd[warp * V + q * EPC + e] = cs.part[e];
+        }
+      }
     }
     __syncthreads();
     // tile j-2's stage was last read by pass 2 in the previous iteration
     if (tid == 0 && j >= 2 && j - 2 + p.stages < my_tiles) issue(j - 2 + p.stages);
-    if (have) finalize(j, (int)(j & 1));
+    if (have)
+      finalize_tile<V>(p, rd, (blockIdx.x + j * G) * (int64_t)V, sS + (j & 1) * V,
+                       sW + (j & 1) * V, mode != MODE_MASS, col_acc);
     if (j >= 1) pass2(tiles + (size_t)s_prev * p.stage_bytes, (int)((j - 1) & 1));
     s_prev = s_cur;
     if (++s_cur == p.stages) { s_cur = 0; par ^= 1u; }
   }
 
-  // ------------------------------------------------ CTA partials -> global
-  // part layout: [grid][p.part_ncb * n][2]
-  if constexpr (ROWS > 0) {
+  // rows -> global partials (part layout [grid][n][2])
 #pragma unroll
-    for (int k = 0; k < ROWS; ++k) {
-      const int r = warp + k * kWarps;
-      const double a = warp_sum(acc_row[k]);
-      const double b = warp_sum(acc_mass[k]);
-      int nb = acc_nb[k];
+  for (int k = 0; k < ROWS; ++k) {
+    const int r = warp + k * kWarps;
+    const double a = warp_sum(acc_row[k]);
+    const double b = warp_sum(acc_mass[k]);
+    int nb = acc_nb[k];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
-      if (lane == 0 && r < n) {
-        double* dst = p.part + ((size_t)blockIdx.x * n + r) * 2;
-        dst[0] = a;
-        dst[1] = b;
-        if (p.mode == MODE_MASS && p.part_nb != nullptr) p.part_nb[(size_t)blockIdx.x * n + r] = nb;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      const int it = tid + k * kThreads;
-      if (it < items) {
-        double* dst = p.part + ((size_t)blockIdx.x * items + it) * 2;
-        dst[0] = acc_row[k];
-        dst[1] = acc_mass[k];
-      }
-    }
-    if (p.mode == MODE_MASS && p.part_nb != nullptr) {
-      // integers: merge the column boxes of one member exactly, any order
-      int64_t* nbp = p.part_nb + (size_t)blockIdx.x * n;
-#pragma unroll
-      for (int k = 0; k < IPT; ++k) {
-        const int it = tid + k * kThreads;
-        if (it < n) nbp[it] = acc_nb[k];
-      }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < IPT; ++k) {
-        const int it = tid + k * kThreads;
-        if (it >= n && it < items)
-          atomicAdd(reinterpret_cast<unsigned long long*>(&nbp[it % n]),
-                    (unsigned long long)acc_nb[k]);
-      }
+    for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    if (lane == 0 && r < n) {
+      double* dst = p.part + ((size_t)blockIdx.x * n + r) * 2;
+      dst[0] = a;
+      dst[1] = b;
+      if (p.mode == MODE_MASS && p.part_nb != nullptr) p.part_nb[(size_t)blockIdx.x * n + r] = nb;
     }
   }
-  constexpr int PNCB = ROWS > 0 ? 1 : NCB;
-  finish_partials(p, PNCB, col_acc, s_ticket, s_col);
+  finish_partials(p, 1, col_acc, s_ticket, s_col);
 }
 
 // ---------------------------------------------------------------------------
-// Large-N variant (n > 256): a tile is V = 2 x 128 B of cells (256 bytes per
-// member row, DRAM-friendly) for ALL members, streamed through SMEM in
-// 256-row chunks twice: touch 1 (column sweep) from HBM with an L2
-// evict_last hint, touch 2 (row sweep) re-reads the same chunks, served by
-// L2.  HBM traffic stays one read of the ensemble.  Thread t owns line
-// (column box t>>8, row t&255) of every chunk; its row sums for chunk c stay
-// in registers (acc[c], c < CMAX).
+// chunked_kernel: 256 < n <= 256 * CMAX.  Thread t owns half (t >> 8) of row
+// (t & 255) of every chunk; it reads the half's 8 chunks in a row-rotated
+// order (bank-conflict free without swizzle) and keeps its row sums for chunk
+// c in registers (acc[c]).
 constexpr int kChunkRows = 256;
-constexpr int kChunkBytes = 2 * kChunkRows * 128;  // 64 KB
+constexpr int kChunkBytes = kChunkRows * kRowBytes;  // 64 KB
 constexpr int kChunkBufs = 3;
 
 template <typename T, int CMAX>
 __global__ void __launch_bounds__(kThreads, 1)
-    chunked_pass_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
+    chunked_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
   constexpr int EPC = Vec<T>::EPC;
-  constexpr int E = 128 / (int)sizeof(T);  // cells per 128-byte line
-  constexpr int V = 2 * E;                 // cells per tile
-  constexpr int P = kThreads / 16;         // row phases in touch 1 (16 chunk columns)
-  static_assert(kThreads == 2 * kChunkRows, "one (box, row) line per thread");
+  constexpr int V = kRowBytes / (int)sizeof(T);
+  constexpr int HALF = V / 2;  // cells per half row
+  static_assert(kThreads == 2 * kChunkRows, "one half row per thread");
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
@@ -530,22 +402,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
 
-  auto issue = [&](int64_t q) {  // q-th chunk load of this CTA
-    const int b = (int)(q % kChunkBufs);
-    const int64_t j = q / loads_per_tile;
-    const int i = (int)(q - j * loads_per_tile);
+  auto issue = [&](int64_t qq) {  // qq-th chunk load of this CTA (thread 0)
+    const int b = (int)(qq % kChunkBufs);
+    const int64_t j = qq / loads_per_tile;
+    const int i = (int)(qq - j * loads_per_tile);
     const bool second = i >= C;
     const int c = second ? i - C : i;
-    const int64_t tile = blockIdx.x + j * G;
-    unsigned char* dst = bufs + (size_t)b * kChunkBytes;
     mbar_arrive_expect_tx(&full[b], kChunkBytes);
-    const uint64_t pol = (two_touch && !second) ? pol_keep : pol_drop;
-    for (int cb = 0; cb < 2; ++cb)
-      tma_load_2d(dst + cb * (kChunkRows * 128), &tmap, (int32_t)(tile * V + cb * E),
-                  c * kChunkRows, &full[b], pol);
+    tma_load_2d(bufs + (size_t)b * kChunkBytes, &tmap, (int32_t)((blockIdx.x + j * G) * V),
+                c * kChunkRows, &full[b], (two_touch && !second) ? pol_keep : pol_drop);
   };
   if (tid == 0)
-    for (int64_t q = 0; q < total_loads && q < kChunkBufs; ++q) issue(q);
+    for (int64_t qq = 0; qq < total_loads && qq < kChunkBufs; ++qq) issue(qq);
 
   double acc_row[CMAX], acc_mass[CMAX];
   int acc_nb[CMAX];
@@ -553,104 +421,46 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int c = 0; c < CMAX; ++c) { acc_row[c] = 0.0; acc_mass[c] = 0.0; acc_nb[c] = 0; }
   double col_acc = 0.0;
 
-  // touch-1 coordinates: chunk column q16 (box, chunk), row phase ph
-  const int q16 = tid & 15, ph = tid >> 4;
-  const int a_cb = q16 >> 3, a_ch = q16 & 7;
-  const uint32_t a_off = (uint32_t)(a_cb * kChunkRows * 128 + ph * 128) +
-                         ((uint32_t)(a_ch ^ (ph & 7)) << 4);
-  // touch-2 coordinates: this thread's line
-  const int b_cb = tid >> 8, b_rr = tid & 255;
-  const uint32_t b_off = (uint32_t)(b_cb * kChunkRows * 128 + b_rr * 128);
-  const uint32_t b_xor = (uint32_t)(b_rr & 7);
+  const int q = tid & (kChunks16 - 1), ph = tid / kChunks16;
+  const uint32_t a_off = (uint32_t)(ph * kRowBytes + q * 16);
+  const int b_half = tid >> 8, b_rr = tid & 255;
+  const uint32_t b_off = (uint32_t)(b_rr * kRowBytes + b_half * (kRowBytes / 2));
+  const int b_rot = b_rr & 7;
 
-  int64_t q = 0;  // chunk loads consumed so far
+  int64_t qq = 0;  // chunk loads consumed
   auto next_chunk = [&]() -> const unsigned char* {
-    const int b = (int)(q % kChunkBufs);
-    mbar_wait(&full[b], (uint32_t)((q / kChunkBufs) & 1));
+    const int b = (int)(qq % kChunkBufs);
+    mbar_wait(&full[b], (uint32_t)((qq / kChunkBufs) & 1));
     return bufs + (size_t)b * kChunkBytes;
   };
   auto release_chunk = [&]() {
     __syncthreads();  // everyone is done with this buffer
-    if (tid == 0 && q + kChunkBufs < total_loads) issue(q + kChunkBufs);
-    ++q;
+    if (tid == 0 && qq + kChunkBufs < total_loads) issue(qq + kChunkBufs);
+    ++qq;
   };
 
+  ColSweep<T> cs;
   for (int64_t j = 0; j < my_tiles; ++j) {
     const int64_t x0 = (blockIdx.x + j * G) * (int64_t)V;
-    // ---------------------------------------------------- touch 1 (columns)
-    if (two_touch) {
-      double part[EPC];
-      float2 sh01 = make_float2(1.0f, 1.0f), sh23 = sh01;
-      float2 sc01 = make_float2(0.0f, 0.0f), sc23 = sc01;
-#pragma unroll
-      for (int e = 0; e < EPC; ++e) part[e] = 0.0;
+    if (two_touch) {  // ------------------------------ touch 1: column sweep
+      cs.reset();
       for (int c = 0; c < C; ++c) {
         const unsigned char* st = next_chunk();
-        const unsigned char* pa = st + a_off;
-        if constexpr (sizeof(T) == 4) {
-          if (mode == MODE_MEAN) {
-#pragma unroll
-            for (int k = 0; k < kChunkRows / P; ++k) {
-              const float4 v = Vec<float>::loadf(pa + k * (P * 128));
-              fast2sum_acc2(sh01, sc01, make_float2(v.x, v.y));
-              fast2sum_acc2(sh23, sc23, make_float2(v.z, v.w));
-            }
-          } else {
-#pragma unroll 4
-            for (int k = 0; k < kChunkRows / P; ++k) {
-              const int r = c * kChunkRows + ph + k * P;
-              double v[EPC];
-              Vec<T>::load(pa + k * (P * 128), v);
-              const double iv = r < n ? __ldg(p.inv + r) : 0.0;
-#pragma unroll
-              for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
-            }
-          }
-        } else {
-#pragma unroll 4
-          for (int k = 0; k < kChunkRows / P; ++k) {
-            const int r = c * kChunkRows + ph + k * P;
-            double v[EPC];
-            Vec<T>::load(pa + k * (P * 128), v);
-            const double iv = mode == MODE_MEAN ? 1.0 : (r < n ? __ldg(p.inv + r) : 0.0);
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
-          }
-        }
+        cs.run(st + a_off, ph, kChunkRows, mode, p.inv, c * kChunkRows + ph, n);
         release_chunk();
       }
-      if constexpr (sizeof(T) == 4) {
-        if (mode == MODE_MEAN) {
-          part[0] = ((double)sh01.x - 1.0) + (double)sc01.x;
-          part[1] = ((double)sh01.y - 1.0) + (double)sc01.y;
-          part[2] = ((double)sh23.x - 1.0) + (double)sc23.x;
-          part[3] = ((double)sh23.y - 1.0) + (double)sc23.y;
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < EPC; ++e) part[e] += __shfl_xor_sync(0xffffffffu, part[e], 16);
+      cs.combine(mode);
       if (lane < 16) {
 #pragma unroll
-        for (int e = 0; e < EPC; ++e) red[warp * V + q16 * EPC + e] = part[e];
+        for (int e = 0; e < EPC; ++e) red[warp * V + q * EPC + e] = cs.part[e];
       }
     }
     __syncthreads();
-    for (int v = tid; v < V; v += kThreads) {
-      const int64_t x = x0 + v;
-      const double wx = x < p.m ? (weighted ? __ldg(p.w + x) : 1.0) : 0.0;
-      sW[v] = wx;
-      if (two_touch) {
-        double S = 0.0;
-#pragma unroll
-        for (int k = 0; k < kWarps; ++k) S += red[k * V + v];
-        sS[v] = wx * S;
-        col_acc = fma(wx, S, col_acc);
-      }
-    }
+    finalize_tile<V>(p, red, x0, sS, sW, two_touch, col_acc);
     __syncthreads();
-    // ------------------------------------------------------- touch 2 (rows)
-    const double* S = sS + b_cb * E;
-    const double* W = sW + b_cb * E;
+    // --------------------------------------------------- touch 2: row sweep
+    const double* S = sS + b_half * HALF;
+    const double* W = sW + b_half * HALF;
 #pragma unroll
     for (int c = 0; c < CMAX; ++c) {
       if (c < C) {
@@ -662,9 +472,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int e = 0; e < EPC; ++e) { ar[e] = 0.0; am[e] = 0.0; }
 #pragma unroll
           for (int L = 0; L < 8; ++L) {
+            const int Lr = (L + b_rot) & 7;
             double v[EPC];
-            Vec<T>::load(line + ((L ^ b_xor) << 4), v);
-            const int vb = L * EPC;
+            Vec<T>::load(line + Lr * 16, v);
+            const int vb = Lr * EPC;
             if (mode == MODE_MASS) {
 #pragma unroll
               for (int e = 0; e < EPC; ++e) {
@@ -700,19 +511,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
-  // ------------------------------------------------ CTA partials -> global
+  // halves -> global partials (part layout [grid][2 * n][2])
 #pragma unroll
   for (int c = 0; c < CMAX; ++c) {
     const int r = c * kChunkRows + b_rr;
     if (c < C && r < n) {
-      double* dst = p.part + ((size_t)blockIdx.x * 2 * n + b_cb * n + r) * 2;
+      double* dst = p.part + ((size_t)blockIdx.x * 2 * n + b_half * n + r) * 2;
       dst[0] = acc_row[c];
       dst[1] = acc_mass[c];
     }
   }
   if (p.mode == MODE_MASS && p.part_nb != nullptr) {
     int64_t* nbp = p.part_nb + (size_t)blockIdx.x * n;
-    if (b_cb == 0) {
+    if (b_half == 0) {
 #pragma unroll
       for (int c = 0; c < CMAX; ++c) {
         const int r = c * kChunkRows + b_rr;
@@ -720,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncthreads();
-    if (b_cb == 1) {
+    if (b_half == 1) {
 #pragma unroll
       for (int c = 0; c < CMAX; ++c) {
         const int r = c * kChunkRows + b_rr;
@@ -733,137 +544,87 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------- host side
+constexpr size_t kSmemBudget = 227 * 1024;
+constexpr int kMaxStages = 8;
+constexpr int kChunkMax = 16;  // n <= 4096
+
 struct Plan {
-  int lb, ncb, ipt, rows, boxr, nrb, stages, grid;
   bool chunked;
+  int rows, stages, grid, box_rows;
   uint32_t stage_bytes;
   size_t smem;
   int64_t tiles;
 };
 
-constexpr size_t kSmemBudget = 227 * 1024;
-
-size_t tail_bytes(int V) { return 64 + (size_t)V * 8 * 4 + (size_t)2 * kWarps * V * 8 + 16 + kWarps * 8 + 64; }
-
-constexpr int kChunkMax = 16;  // chunked layout: n <= 4096
-bool use_chunked(int64_t n) { return n > 256 && n <= (int64_t)kChunkMax * kChunkRows; }
-size_t chunked_smem() {
-  return 1024 + (size_t)kChunkBufs * kChunkBytes + 64 + (size_t)(2 + kWarps) * 64 * 8 + 16 +
+size_t rows_tail(int V) {
+  return 128 + (size_t)4 * V * 8 + (size_t)2 * kWarps * V * 8 + 16 + kWarps * 8 + 64;
+}
+size_t chunked_smem(int V) {
+  return 1024 + (size_t)kChunkBufs * kChunkBytes + 64 + (size_t)(2 + kWarps) * V * 8 + 16 +
          kWarps * 8 + 64;
 }
 
 bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
   if (n < 1 || m < 1) return false;
-  pl.chunked = false;
-  if (use_chunked(n)) {  // wide tiles, two touches through L2 (see chunked_pass_kernel)
-    const int V = 2 * 128 / esize;
-    pl.chunked = true;
-    pl.lb = 128; pl.ncb = 2; pl.ipt = 1; pl.rows = 0;
-    pl.boxr = kChunkRows; pl.nrb = (int)((n + kChunkRows - 1) / kChunkRows);
-    pl.stages = kChunkBufs; pl.stage_bytes = kChunkBytes;
-    pl.smem = chunked_smem();
-    pl.tiles = (m + V - 1) / V;
-    pl.grid = (int)std::min<int64_t>(pl.tiles, sm_count());
+  const int V = kRowBytes / esize;
+  pl.tiles = (m + V - 1) / V;
+  pl.grid = (int)std::min<int64_t>(pl.tiles, sm_count());
+  if (n <= 256) {
+    pl.chunked = false;
+    pl.rows = (int)((n + kWarps - 1) / kWarps);
+    pl.box_rows = (int)n;
+    pl.stage_bytes = (uint32_t)align_up((size_t)n * kRowBytes, 1024);
+    const size_t tb = rows_tail(V) + 1024;
+    pl.stages = (int)std::min<size_t>(kMaxStages, (kSmemBudget - tb) / pl.stage_bytes);
+    if (pl.stages < 3) return false;
+    pl.smem = (size_t)pl.stages * pl.stage_bytes + tb;
     return true;
   }
-  const int nrb = (int)((n + 255) / 256);
-  const int boxr_full = (int)(((n + nrb - 1) / nrb + 7) / 8 * 8);
-  const int rows = nrb * boxr_full;
-  struct Cand { int lb, ncb; };
-  const Cand cands[] = {{128, 2}, {128, 1}, {64, 1}, {32, 1}};
-  for (const Cand& c : cands) {
-    const int V = c.ncb * c.lb / esize;
-    const uint32_t sb = (uint32_t)(c.ncb * rows * c.lb);
-    const size_t tb = tail_bytes(V) + 1024;
-    const int min_stages = 3;  // tiles j (pass 1), j-1 (pass 2) and >= 1 in flight
-    int stages = (int)std::min<size_t>(8, (kSmemBudget - tb) / sb);
-    if (sb > kSmemBudget || stages < min_stages) continue;
-    const int64_t items = (int64_t)c.ncb * n;
-    int ipt = 1;
-    while ((int64_t)ipt * kThreads < items) ipt *= 2;
-    if (ipt > (c.lb == 128 ? 2 : (c.lb == 64 ? 4 : 8))) continue;
-    int rows_per_warp = 0;  // row-resident pass 2 for 2x128B-line tiles
-    if (c.lb == 128 && c.ncb == 2) {
-      rows_per_warp = (int)((n + kWarps - 1) / kWarps);
-      if (rows_per_warp > 16) rows_per_warp = 0;
-    }
-    pl.lb = c.lb; pl.ncb = c.ncb; pl.ipt = ipt; pl.rows = rows_per_warp;
-    pl.boxr = boxr_full; pl.nrb = nrb;
-    pl.stages = stages; pl.stage_bytes = sb;
-    pl.smem = (size_t)stages * sb + tb;
-    pl.tiles = (m + V - 1) / V;
-    pl.grid = (int)std::min<int64_t>(pl.tiles, sm_count());
-    return true;
-  }
-  return false;
+  if (n > (int64_t)kChunkMax * kChunkRows) return false;
+  pl.chunked = true;
+  pl.rows = 0;
+  pl.box_rows = kChunkRows;
+  pl.stages = kChunkBufs;
+  pl.stage_bytes = kChunkBytes;
+  pl.smem = chunked_smem(V);
+  return true;
 }
 
 size_t workspace_bytes(const Plan& pl, int64_t n) {
-  const int64_t items = (int64_t)pl.ncb * n;
   size_t b = 256;  // completion counter: fixed offset 0, zero between launches
-  b += align_up((size_t)pl.grid * items * 2 * sizeof(double), 256);
+  b += align_up((size_t)pl.grid * 2 * n * 2 * sizeof(double), 256);
   b += align_up((size_t)pl.grid * sizeof(double), 256);
   b += align_up((size_t)pl.grid * n * sizeof(int64_t), 256);
   return b;
 }
 
-template <typename T, int LB, int NCB, int IPT, int ROWS>
-int launch_t(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream_t st) {
-  auto kern = stream_pass_kernel<T, LB, NCB, IPT, ROWS>;
+template <typename K>
+int launch(K kern, const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream_t st) {
   PIDB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
   kern<<<pl.grid, kThreads, pl.smem, st>>>(tm, sp);
-  PIDB_LAUNCH_CHECK("stream_pass_kernel");
+  PIDB_LAUNCH_CHECK("stream kernel");
   return PIDB_OK;
 }
 
-template <typename T, int LB, int NCB>
-int launch_ipt(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream_t st) {
-  // only the (layout, items-per-thread) pairs make_plan can produce are built
-  if constexpr (LB == 128 && NCB == 2) {
-    switch (pl.rows) {
-#define PIDB_ROWS_CASE(R) case R: return launch_t<T, LB, NCB, 1, R>(tm, sp, pl, st);
-      PIDB_ROWS_CASE(1) PIDB_ROWS_CASE(2) PIDB_ROWS_CASE(3) PIDB_ROWS_CASE(4)
-      PIDB_ROWS_CASE(5) PIDB_ROWS_CASE(6) PIDB_ROWS_CASE(7) PIDB_ROWS_CASE(8)
-      PIDB_ROWS_CASE(9) PIDB_ROWS_CASE(10) PIDB_ROWS_CASE(11) PIDB_ROWS_CASE(12)
-      PIDB_ROWS_CASE(13) PIDB_ROWS_CASE(14) PIDB_ROWS_CASE(15) PIDB_ROWS_CASE(16)
+template <typename T>
+int launch_typed(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream_t st) {
+  if (pl.chunked) {
+    const int C = (int)((sp.n + kChunkRows - 1) / kChunkRows);
+    if (C <= 4) return launch(chunked_kernel<T, 4>, tm, sp, pl, st);
+    if (C <= 8) return launch(chunked_kernel<T, 8>, tm, sp, pl, st);
+    return launch(chunked_kernel<T, 16>, tm, sp, pl, st);
+  }
+  switch (pl.rows) {
+#define PIDB_ROWS_CASE(R) \
+  case R: return launch(rows_kernel<T, R>, tm, sp, pl, st);
+    PIDB_ROWS_CASE(1) PIDB_ROWS_CASE(2) PIDB_ROWS_CASE(3) PIDB_ROWS_CASE(4)
+    PIDB_ROWS_CASE(5) PIDB_ROWS_CASE(6) PIDB_ROWS_CASE(7) PIDB_ROWS_CASE(8)
+    PIDB_ROWS_CASE(9) PIDB_ROWS_CASE(10) PIDB_ROWS_CASE(11) PIDB_ROWS_CASE(12)
+    PIDB_ROWS_CASE(13) PIDB_ROWS_CASE(14) PIDB_ROWS_CASE(15) PIDB_ROWS_CASE(16)
 #undef PIDB_ROWS_CASE
-    }
   }
-  constexpr int kMaxIpt = LB == 128 ? 2 : (LB == 64 ? 4 : 8);
-  switch (pl.ipt) {
-    case 1: return launch_t<T, LB, NCB, 1, 0>(tm, sp, pl, st);
-    case 2: return launch_t<T, LB, NCB, 2, 0>(tm, sp, pl, st);
-    case 4: if constexpr (kMaxIpt >= 4) return launch_t<T, LB, NCB, 4, 0>(tm, sp, pl, st); break;
-    case 8: if constexpr (kMaxIpt >= 8) return launch_t<T, LB, NCB, 8, 0>(tm, sp, pl, st); break;
-  }
-  set_error("unsupported items-per-thread %d for %d-byte lines", pl.ipt, LB);
+  set_error("unsupported rows per warp %d", pl.rows);
   return PIDB_EUNSUPPORTED;
-}
-
-template <typename T>
-int launch_layout(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream_t st) {
-  if (pl.lb == 128 && pl.ncb == 2) return launch_ipt<T, 128, 2>(tm, sp, pl, st);
-  if (pl.lb == 128 && pl.ncb == 1) return launch_ipt<T, 128, 1>(tm, sp, pl, st);
-  if (pl.lb == 64) return launch_ipt<T, 64, 1>(tm, sp, pl, st);
-  return launch_ipt<T, 32, 1>(tm, sp, pl, st);
-}
-
-template <typename T, int CMAX>
-int launch_chunked_t(const CUtensorMap& tm, StreamParams& sp, int grid, cudaStream_t st) {
-  auto kern = chunked_pass_kernel<T, CMAX>;
-  const size_t smem = chunked_smem();
-  PIDB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<grid, kThreads, smem, st>>>(tm, sp);
-  PIDB_LAUNCH_CHECK("chunked_pass_kernel");
-  return PIDB_OK;
-}
-
-template <typename T>
-int launch_chunked(const CUtensorMap& tm, StreamParams& sp, int grid, cudaStream_t st) {
-  const int C = (int)((sp.n + kChunkRows - 1) / kChunkRows);
-  if (C <= 4) return launch_chunked_t<T, 4>(tm, sp, grid, st);
-  if (C <= 8) return launch_chunked_t<T, 8>(tm, sp, grid, st);
-  return launch_chunked_t<T, 16>(tm, sp, grid, st);
 }
 
 int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
@@ -874,13 +635,13 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
   PIDB_REQUIRE(n >= 1 && m >= 1, "need n >= 1 members and m >= 1 cells (got %lld, %lld)",
                (long long)n, (long long)m);
   const int es = dtype == PIDB_F32 ? 4 : 8;
-  PIDB_REQUIRE(ld >= m && (ld * es) % 16 == 0, "row stride %lld must be >= m and a multiple of 16 bytes",
-               (long long)ld);
+  PIDB_REQUIRE(ld >= m && (ld * es) % 16 == 0,
+               "row stride %lld must be >= m and a multiple of 16 bytes", (long long)ld);
   PIDB_REQUIRE((reinterpret_cast<uintptr_t>(u) & 15) == 0, "member matrix must be 16-byte aligned");
-  PIDB_REQUIRE(n <= INT32_MAX, "too many members");
   Plan pl;
   if (!make_plan(n, m, es, pl)) {
-    set_error("ensemble with %lld members does not fit the single-pass tile layout", (long long)n);
+    set_error("ensembles of %lld members are not supported by the streaming tile (max %d)",
+              (long long)n, kChunkMax * kChunkRows);
     return PIDB_EUNSUPPORTED;
   }
   const size_t need = workspace_bytes(pl, n);
@@ -889,35 +650,28 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
     return PIDB_EWORKSPACE;
   }
   CUtensorMap tm;
-  int rc = encode_tma_2d(&tm, u, dtype == PIDB_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
-                                                     : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
-                         (uint64_t)m, (uint64_t)n, (uint64_t)ld * es, (uint32_t)(pl.lb / es),
-                         (uint32_t)pl.boxr,
-                         pl.lb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                      : (pl.lb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                     : CU_TENSOR_MAP_SWIZZLE_32B));
+  int rc = encode_tma_2d(&tm, u,
+                         dtype == PIDB_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                           : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                         (uint64_t)m, (uint64_t)n, (uint64_t)ld * es, (uint32_t)(kRowBytes / es),
+                         (uint32_t)pl.box_rows, CU_TENSOR_MAP_SWIZZLE_NONE);
   if (rc != PIDB_OK) return rc;
-  const int64_t items = (int64_t)pl.ncb * n;
   char* base = static_cast<char*>(ws);
   StreamParams sp{};
   sp.counter = reinterpret_cast<unsigned*>(base);
   base += 256;
-  sp.n = n; sp.m = m; sp.tiles = pl.tiles; sp.nrb = pl.nrb; sp.boxr = pl.boxr;
+  sp.n = n; sp.m = m; sp.tiles = pl.tiles;
   sp.stages = pl.stages; sp.stage_bytes = pl.stage_bytes; sp.mode = mode;
   sp.w = w; sp.inv = inv;
   sp.part = reinterpret_cast<double*>(base);
-  base += align_up((size_t)pl.grid * items * 2 * sizeof(double), 256);
+  base += align_up((size_t)pl.grid * 2 * n * 2 * sizeof(double), 256);
   sp.part_col = reinterpret_cast<double*>(base);
   base += align_up((size_t)pl.grid * sizeof(double), 256);
   sp.part_nb = out_nb ? reinterpret_cast<int64_t*>(base) : nullptr;
-  base += align_up((size_t)pl.grid * n * sizeof(int64_t), 256);
   sp.out_row = out_row; sp.out_mass = out_mass; sp.out_col = out_col; sp.out_nb = out_nb;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (pl.chunked)
-    return dtype == PIDB_F32 ? launch_chunked<float>(tm, sp, pl.grid, st)
-                             : launch_chunked<double>(tm, sp, pl.grid, st);
-  return dtype == PIDB_F32 ? launch_layout<float>(tm, sp, pl, st)
-                           : launch_layout<double>(tm, sp, pl, st);
+  return dtype == PIDB_F32 ? launch_typed<float>(tm, sp, pl, st)
+                           : launch_typed<double>(tm, sp, pl, st);
 }
 
 }  // namespace
