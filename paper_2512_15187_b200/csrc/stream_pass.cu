@@ -199,19 +199,27 @@ __device__ __forceinline__ void finish_partials(const StreamParams& p, int pncb,
 }
 
 // sS/sW for tile cells [x0, x0+V): w*S (or w*T) and w; col_acc += w*S.
-template <int V>
+// EPC_PERM > 0 stores cell (8 chunks of EPC per half row) at the
+// element-major slot half*V/2 + e*8 + chunk, which makes the chunked
+// kernel's row-rotated reads bank-conflict free.
+template <int V, int EPC_PERM>
 __device__ __forceinline__ void finalize_tile(const StreamParams& p, const double* rd, int64_t x0,
                                               double* sS, double* sW, bool colsum,
                                               double& col_acc) {
   for (int v = threadIdx.x; v < V; v += kThreads) {
     const int64_t x = x0 + v;
     const double wx = x < p.m ? (p.w ? __ldg(p.w + x) : 1.0) : 0.0;
-    sW[v] = wx;
+    int slot = v;
+    if constexpr (EPC_PERM > 0) {
+      const int half = v / (V / 2), hv = v % (V / 2);
+      slot = half * (V / 2) + (hv % EPC_PERM) * 8 + hv / EPC_PERM;
+    }
+    sW[slot] = wx;
     if (colsum) {
       double S = 0.0;
 #pragma unroll
       for (int k = 0; k < kWarps; ++k) S += rd[k * V + v];
-      sS[v] = wx * S;
+      sS[slot] = wx * S;
       col_acc = fma(wx, S, col_acc);
     }
   }
@@ -329,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // tile j-2's stage was last read by pass 2 in the previous iteration
     if (tid == 0 && j >= 2 && j - 2 + p.stages < my_tiles) issue(j - 2 + p.stages);
     if (have)
-      finalize_tile<V>(p, rd, (blockIdx.x + j * G) * (int64_t)V, sS + (j & 1) * V,
+      finalize_tile<V, 0>(p, rd, (blockIdx.x + j * G) * (int64_t)V, sS + (j & 1) * V,
                        sW + (j & 1) * V, mode != MODE_MASS, col_acc);
     if (j >= 1) pass2(tiles + (size_t)s_prev * p.stage_bytes, (int)((j - 1) & 1));
     s_prev = s_cur;
@@ -456,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncthreads();
-    finalize_tile<V>(p, red, x0, sS, sW, two_touch, col_acc);
+    finalize_tile<V, EPC>(p, red, x0, sS, sW, two_touch, col_acc);
     __syncthreads();
     // --------------------------------------------------- touch 2: row sweep
     const double* S = sS + b_half * HALF;
@@ -475,26 +483,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int Lr = (L + b_rot) & 7;
             double v[EPC];
             Vec<T>::load(line + Lr * 16, v);
-            const int vb = Lr * EPC;
+            // element-major S/W slots (finalize_tile<V, EPC>): e*8 + chunk
             if (mode == MODE_MASS) {
 #pragma unroll
               for (int e = 0; e < EPC; ++e) {
-                am[e] = fma(v[e], W[vb + e], am[e]);
+                am[e] = fma(v[e], W[e * 8 + Lr], am[e]);
                 nb += is_nonbinary(v[e]);
               }
             } else if (mode == MODE_COLS) {
 #pragma unroll
-              for (int e = 0; e < EPC; ++e) ar[e] = fma(v[e], S[vb + e], ar[e]);
+              for (int e = 0; e < EPC; ++e) ar[e] = fma(v[e], S[e * 8 + Lr], ar[e]);
             } else if (weighted) {
 #pragma unroll
               for (int e = 0; e < EPC; ++e) {
-                ar[e] = fma(v[e], S[vb + e], ar[e]);
-                am[e] = fma(v[e], W[vb + e], am[e]);
+                ar[e] = fma(v[e], S[e * 8 + Lr], ar[e]);
+                am[e] = fma(v[e], W[e * 8 + Lr], am[e]);
               }
             } else {
 #pragma unroll
               for (int e = 0; e < EPC; ++e) {
-                ar[e] = fma(v[e], S[vb + e], ar[e]);
+                ar[e] = fma(v[e], S[e * 8 + Lr], ar[e]);
                 am[e] += v[e];
               }
             }
