@@ -345,9 +345,11 @@ def run_ours(args, rank, world, local, pg):
             else e2e_meta
         del host
 
-    # ---------------- secondary: exact PID on cfg4
+    # ---------------- secondary: exact PID on cfg4, bit-exact eID on cfg2
     if args.workload == "cfg5" and not args.no_pid:
         line["pid"] = run_pid_secondary(args, rank, world, pg, dev, pk)
+    if args.workload == "cfg5" and not args.no_eid and world == 1:
+        line["eid"] = run_eid_secondary(args, dev, pk)
 
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -451,6 +453,43 @@ def run_pid_secondary(args, rank, world, pg, dev, pk):
     return out
 
 
+def run_eid_secondary(args, dev, pk):
+    """cfg2: eID on 500 binary Fourier contours 512^2 (reference generator),
+    bit-exact integer path: K6 binary check + K7 pack + K2 tcgen05 i8 Gram +
+    exact epilogue."""
+    import torch
+
+    import paper_2512_15187_b200 as pb
+    from paper_2512_15187_b200 import depth as D
+    from paper_2512_15187_b200 import synth
+
+    n, res = 500, 512
+    de = synth.contours_device(n, res, 0, device=dev)
+    torch.cuda.synchronize()
+    D.KERNEL_EVENTS = []
+    pb.depth_eid(de)
+    D.KERNEL_EVENTS = []
+    ms = timed(lambda: pb.depth_eid(de), max(1, min(args.steps, 10)), 3, 1)
+    ev = D.KERNEL_EVENTS
+    D.KERNEL_EVENTS = None
+    kg, _ = kernel_ms(ev, "pidb_gram_i8")
+    km, _ = kernel_ms(ev, "pidb_member_masses")
+    m = res * res
+    ops = 2.0 * n * n * m
+    out = {"workload": "cfg2: eID, 500 binary contours 512^2 (bit-exact integer path)",
+           "ms_per_depth": ms, "value": n * m / (ms * 1e-3), "unit": "member-voxels/s",
+           "pair_voxels_per_s": n * n * m / (ms * 1e-3),
+           "gram_roofline": {"bound": "tensor", "kernel": "gram_i8_kernel (+int64 reduce)",
+                             "achieved": ops / (kg * 1e-3) / 1e12, "unit": "TOP/s",
+                             "peak": INT8_TOPS_PROBE, "frac": ops / (kg * 1e-3) / 1e12 / INT8_TOPS_PROBE,
+                             "kernel_ms": kg, "algorithmic_ops": ops,
+                             "peak_src": "cuBLAS INT8 probe (torch._int_mm 8192^3)"},
+           "masses_ms": km}
+    del de
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -461,6 +500,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pid", action="store_true")
+    ap.add_argument("--no-eid", action="store_true")
     ap.add_argument("--ref-planes", type=int, default=0)
     ap.add_argument("--ref-pid-members", type=int, default=64)
     args = ap.parse_args()

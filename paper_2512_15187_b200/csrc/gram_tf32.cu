@@ -15,8 +15,9 @@
 //
 // Work: 128x128 output tiles of the upper block triangle x split-K cell
 // ranges; fp64 split partials are reduced (fixed order) and mirrored by a
-// second kernel.  Warps (320 threads): 0 TMA producer, 1 MMA issuer,
-// 2-5 converters, 6-9 epilogue (one TMEM lane quadrant each).
+// second kernel.  Warps (672 threads): 0 MMA issuer, 1-4 epilogue (one TMEM
+// lane quadrant each), 5-20 converters (LDG.128 operand loads, two stages
+// in flight in registers, hi/lo split written to the swizzled stages).
 #include "tcgen05.cuh"
 
 namespace pidb {
@@ -27,16 +28,22 @@ constexpr int kBK = 32;            // fp32 cells per stage (one 128-byte line)
 constexpr int kStages = 3;
 constexpr int kFlushStages = 16;   // 512 cells per fp32 accumulation block
 constexpr int kTileBytes = kB * kBK * 4;             // 16 KB
-constexpr int kStageBytes = 4 * kTileBytes;          // A, B, A_lo, B_lo
-constexpr int kThreads = 320;
-constexpr int kConvThreads = 128;
+constexpr int kStageBytes = 4 * kTileBytes;          // A_hi, B_hi, A_lo, B_lo
+constexpr int kConvWarps = 16;
+constexpr int kConvThreads = kConvWarps * 32;        // 512
+constexpr int kEpiWarp0 = 1;                         // warps 1..4: epilogue
+constexpr int kConvWarp0 = 5;                        // warps 5..20: converters
+constexpr int kThreads = (kConvWarp0 + kConvWarps) * 32;  // 672
+constexpr int kChunksPerTile = kB * kBK / 4;         // 16-byte chunks per operand tile
+constexpr int kCPT = kChunksPerTile / kConvThreads;  // chunks per converter thread (2)
 constexpr uint32_t kIdesc = tc::idesc(tc::kCF32, tc::kTF32, kB, kB);
 // TMEM columns: [0,128) acc0, [128,256) acc1, [256,512) fp64 shadow (lo,hi pairs)
 constexpr uint32_t kTmemCols = 512;
 
 struct GramTf32Params {
   int n, nb, ntiles, splits, kblocks, kb_per;
-  int64_t m;
+  int64_t m, ld;
+  const float* u;
   const double* w;   // nullable
   double* part;      // [units][kB][kB]
 };
@@ -50,18 +57,26 @@ __device__ __forceinline__ void tile_of(int t, int& ib, int& jb) {
   ib = t;
 }
 
+// Operands are fetched by the converter warps themselves with coalesced
+// 128-bit loads (a warp reads four whole 128-byte member lines): TMA boxes
+// with 128-byte rows are capped at ~16 B/clk/SM (tools/ubench_tma.cu), below
+// what the tensor cores consume.  Each chunk is written twice into the
+// 128B-swizzled K-major stage: hi (the raw fp32 word, which the tensor core
+// truncates to tf32, or rna(w*u) when weighted) and lo = rna(a - hi).
+struct OperandChunks {
+  float4 v[2][kCPT];  // [A/B][chunk]
+};
+
 __global__ void __launch_bounds__(kThreads, 1)
-    gram_tf32_kernel(const __grid_constant__ CUtensorMap tmap, const GramTf32Params p) {
+    gram_tf32_kernel(const GramTf32Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   unsigned char* ring = smem_raw + pad;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kStages * kStageBytes);
-  uint64_t* conv = full + kStages;
+  uint64_t* conv = reinterpret_cast<uint64_t*>(ring + kStages * kStageBytes);
   uint64_t* empty = conv + kStages;
   uint64_t* acc_full = empty + kStages;   // [2]
   uint64_t* acc_empty = acc_full + 2;     // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  double* wst = reinterpret_cast<double*>(tmem_slot + 2);  // [kStages][kBK] weights
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = blockIdx.x;
@@ -77,9 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nflush = (nk + kFlushStages - 1) / kFlushStages;
 
   if (threadIdx.x == 0) {
-    prefetch_tma_desc(&tmap);
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
       mbar_init(&conv[s], kConvThreads);
       mbar_init(&empty[s], 1);
     }
@@ -89,30 +102,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 6) tc::tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == kEpiWarp0) tc::tmem_alloc(tmem_slot, kTmemCols);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    if (tc::elect_one()) {
-      const uint64_t pol = policy_evict_last();
-      const uint32_t bytes = share_b ? kTileBytes : 2 * kTileBytes;
-      int s = 0;
-      uint32_t ph = 0;
-      for (int k = 0; k < nk; ++k) {
-        mbar_wait(&empty[s], ph ^ 1u);
-        unsigned char* st = ring + s * kStageBytes;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        const int x = (kb0 + k) * kBK;
-        tma_load_2d(st, &tmap, x, ib * kB, &full[s], pol);
-        if (!share_b) tma_load_2d(st + kTileBytes, &tmap, x, jb * kB, &full[s], pol);
-        if (++s == kStages) { s = 0; ph ^= 1u; }
-      }
-    }
-  } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
     if (tc::elect_one()) {
       int s = 0;
@@ -147,60 +143,96 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::commit(&acc_full[buf]);
       }
     }
-  } else if (warp < 6) {
+  } else if (warp >= kConvWarp0) {
     // ----------------------------------------------------------- converters
-    const int ct = threadIdx.x - 64;  // 0..127
+    const int ct = threadIdx.x - kConvWarp0 * 32;  // 0..511
+    const int nops = share_b ? 1 : 2;
+    // chunk c = ct + q * 512: line r = c >> 3, chunk ch = c & 7 (logical)
+    auto load = [&](int k, OperandChunks& oc) {
+      const int64_t x0 = (int64_t)(kb0 + k) * kBK;
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        if (o >= nops) break;
+        const int rb = (o == 0 ? ib : jb) * kB;
+#pragma unroll
+        for (int q = 0; q < kCPT; ++q) {
+          const int c = ct + q * kConvThreads;
+          const int r = c >> 3, ch = c & 7;
+          const int64_t x = x0 + ch * 4;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (rb + r < p.n) {
+            const float* src = p.u + (int64_t)(rb + r) * p.ld + x;
+            if (x + 4 <= p.m) {
+              v = __ldcg(reinterpret_cast<const float4*>(src));
+            } else {
+              if (x + 0 < p.m) v.x = src[0];
+              if (x + 1 < p.m) v.y = src[1];
+              if (x + 2 < p.m) v.z = src[2];
+            }
+          }
+          oc.v[o][q] = v;
+        }
+      }
+    };
+    auto store = [&](int k, int s, const OperandChunks& oc) {
+      unsigned char* st = ring + s * kStageBytes;
+      const int64_t x0 = (int64_t)(kb0 + k) * kBK;
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        if (o >= nops) break;
+#pragma unroll
+        for (int q = 0; q < kCPT; ++q) {
+          const int c = ct + q * kConvThreads;
+          const int r = c >> 3, ch = c & 7;
+          const uint32_t off = (uint32_t)(r * 128) + ((uint32_t)(ch ^ (r & 7)) << 4);
+          float4 v = oc.v[o][q];
+          float4 hi;
+          if (o == 0 && weighted) {
+            const int64_t x = x0 + ch * 4;
+            v.x = (float)((double)v.x * (x + 0 < p.m ? __ldg(p.w + x + 0) : 0.0));
+            v.y = (float)((double)v.y * (x + 1 < p.m ? __ldg(p.w + x + 1) : 0.0));
+            v.z = (float)((double)v.z * (x + 2 < p.m ? __ldg(p.w + x + 2) : 0.0));
+            v.w = (float)((double)v.w * (x + 3 < p.m ? __ldg(p.w + x + 3) : 0.0));
+            hi = make_float4(tc::tf32_rna(v.x), tc::tf32_rna(v.y), tc::tf32_rna(v.z),
+                             tc::tf32_rna(v.w));
+          } else {
+            hi = v;  // the tensor core reads tf32 = truncation of this word
+            v = make_float4(tc::tf32_trunc(v.x), tc::tf32_trunc(v.y), tc::tf32_trunc(v.z),
+                            tc::tf32_trunc(v.w));
+            v = make_float4(hi.x - v.x, hi.y - v.y, hi.z - v.z, hi.w - v.w);  // exact remainder
+            *reinterpret_cast<float4*>(st + o * kTileBytes + off) = hi;
+            *reinterpret_cast<float4*>(st + (2 + o) * kTileBytes + off) =
+                make_float4(tc::tf32_rna(v.x), tc::tf32_rna(v.y), tc::tf32_rna(v.z),
+                            tc::tf32_rna(v.w));
+            continue;
+          }
+          *reinterpret_cast<float4*>(st + o * kTileBytes + off) = hi;
+          *reinterpret_cast<float4*>(st + (2 + o) * kTileBytes + off) =
+              make_float4(tc::tf32_rna(v.x - hi.x), tc::tf32_rna(v.y - hi.y),
+                          tc::tf32_rna(v.z - hi.z), tc::tf32_rna(v.w - hi.w));
+        }
+      }
+    };
+    // two stages of loads in flight in registers
+    OperandChunks r0, r1;
+    if (nk > 0) load(0, r0);
+    if (nk > 1) load(1, r1);
     int s = 0;
     uint32_t ph = 0;
-    for (int k = 0; k < nk; ++k) {
-      mbar_wait(&full[s], ph);
-      unsigned char* st = ring + s * kStageBytes;
-      const int x0 = (kb0 + k) * kBK;
-      double* ws = wst + s * kBK;
-      if (weighted) {
-        if (ct < kBK) ws[ct] = (x0 + ct) < p.m ? __ldg(p.w + x0 + ct) : 0.0;
-        asm volatile("bar.sync 1, %0;" ::"n"(kConvThreads) : "memory");
-      }
-      // A tile: 1024 16-byte chunks; chunk c = line r = c/8, physical slot c%8
-#pragma unroll 4
-      for (int c = ct; c < kB * 8; c += kConvThreads) {
-        float4* src = reinterpret_cast<float4*>(st + c * 16);
-        float4* lo = reinterpret_cast<float4*>(st + 2 * kTileBytes + c * 16);
-        float4 v = *src;
-        if (weighted) {
-          const int r = c >> 3;
-          const int lc = (c & 7) ^ (r & 7);  // logical chunk -> cells 4*lc..4*lc+3
-          const double* wc = ws + 4 * lc;
-          v.x = (float)((double)v.x * wc[0]);
-          v.y = (float)((double)v.y * wc[1]);
-          v.z = (float)((double)v.z * wc[2]);
-          v.w = (float)((double)v.w * wc[3]);
-          float4 h = make_float4(tc::tf32_rna(v.x), tc::tf32_rna(v.y), tc::tf32_rna(v.z),
-                                 tc::tf32_rna(v.w));
-          *src = h;
-          *lo = make_float4(tc::tf32_rna(v.x - h.x), tc::tf32_rna(v.y - h.y),
-                            tc::tf32_rna(v.z - h.z), tc::tf32_rna(v.w - h.w));
-        } else {
-          *lo = make_float4(tc::tf32_rna(v.x - tc::tf32_trunc(v.x)),
-                            tc::tf32_rna(v.y - tc::tf32_trunc(v.y)),
-                            tc::tf32_rna(v.z - tc::tf32_trunc(v.z)),
-                            tc::tf32_rna(v.w - tc::tf32_trunc(v.w)));
-        }
-      }
-      if (!share_b) {
-#pragma unroll 4
-        for (int c = ct; c < kB * 8; c += kConvThreads) {
-          const float4 v = *reinterpret_cast<const float4*>(st + kTileBytes + c * 16);
-          *reinterpret_cast<float4*>(st + 3 * kTileBytes + c * 16) =
-              make_float4(tc::tf32_rna(v.x - tc::tf32_trunc(v.x)),
-                          tc::tf32_rna(v.y - tc::tf32_trunc(v.y)),
-                          tc::tf32_rna(v.z - tc::tf32_trunc(v.z)),
-                          tc::tf32_rna(v.w - tc::tf32_trunc(v.w)));
-        }
-      }
+    for (int k = 0; k < nk; k += 2) {
+      mbar_wait(&empty[s], ph ^ 1u);
+      store(k, s, r0);
       fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.mma
       mbar_arrive(&conv[s]);
       if (++s == kStages) { s = 0; ph ^= 1u; }
+      if (k + 2 < nk) load(k + 2, r0);
+      if (k + 1 >= nk) break;
+      mbar_wait(&empty[s], ph ^ 1u);
+      store(k + 1, s, r1);
+      fence_proxy_async_smem();
+      mbar_arrive(&conv[s]);
+      if (++s == kStages) { s = 0; ph ^= 1u; }
+      if (k + 3 < nk) load(k + 3, r1);
     }
   } else {
     // ------------------------------------------------------------- epilogue
@@ -259,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 6) tc::tmem_dealloc(tmem, kTmemCols);
+  if (warp == kEpiWarp0) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
 // G[i][j] = G[j][i] = sum over splits (fixed order) of the tile holding (min, max).
@@ -294,7 +326,7 @@ Plan plan(int64_t n, int64_t m) {
   g.kb_per = (g.kblocks + g.splits - 1) / g.splits;
   g.splits = (g.kblocks + g.kb_per - 1) / g.kb_per;
   g.units = g.ntiles * g.splits;
-  g.smem = 1024 + (size_t)kStages * kStageBytes + 256 + kStages * kBK * sizeof(double);
+  g.smem = 1024 + (size_t)kStages * kStageBytes + 256;
   g.ws = 256 + (size_t)g.units * kB * kB * sizeof(double);
   return g;
 }
@@ -317,18 +349,14 @@ extern "C" int pidb_gram_tf32x3(const float* u, int64_t n, int64_t m, int64_t ld
   PIDB_REQUIRE(n <= (1 << 16), "too many members for the dense Gram");
   const Plan g = plan(n, m);
   PIDB_REQUIRE(ws && ws_bytes >= g.ws, "workspace too small: need %zu bytes", g.ws);
-  CUtensorMap tm;
-  int rc = encode_tma_2d(&tm, u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)m, (uint64_t)n,
-                         (uint64_t)ld * 4, kBK, kB, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (rc != PIDB_OK) return rc;
   GramTf32Params p{};
   p.n = (int)n; p.nb = g.nb; p.ntiles = g.ntiles; p.splits = g.splits; p.kblocks = g.kblocks;
-  p.kb_per = g.kb_per; p.m = m; p.w = w;
+  p.kb_per = g.kb_per; p.m = m; p.ld = ld; p.u = u; p.w = w;
   p.part = reinterpret_cast<double*>(static_cast<char*>(ws) + 256);
   cudaStream_t st = (cudaStream_t)stream;
   PIDB_CUDA(cudaFuncSetAttribute(gram_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)g.smem));
-  gram_tf32_kernel<<<g.units, kThreads, g.smem, st>>>(tm, p);
+  gram_tf32_kernel<<<g.units, kThreads, g.smem, st>>>(p);
   PIDB_LAUNCH_CHECK("gram_tf32_kernel");
   const int64_t total = n * n;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
