@@ -144,10 +144,11 @@ int pidb_inverse_masses(int64_t n, const double* mass, double* inv, void* stream
 /* eID exact epilogue from the integer Gram (unit weights): per pair
  * term = 1.0 - (double)(I[i,i]-I[i,j]) / (double)I[i,i]  (0 if I[i,i]==0),
  * row/col sums exactly rounded (128-bit fixed point == math.fsum), then / n.
- * Bit-identical to ref_eid (/root/reference/pkg/tests/reference_impl.py:60-70). */
+ * Bit-identical to ref_eid (/root/reference/pkg/tests/reference_impl.py:60-70).
+ * mass (nullable, n doubles) receives the member masses I[i,i]. */
 int pidb_eid_exact_epilogue(const int64_t* gram, int64_t n, double* in_in,
                             double* in_out, double* depth, int64_t* rank,
-                            void* stream);
+                            double* mass, void* stream);
 
 /* eID epilogue from factorised sums (weighted binary ensembles):
  * row_excess = n*m_i - row_plain[i], col excess = n_pos - col_inv[j], then

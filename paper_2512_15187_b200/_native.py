@@ -53,7 +53,7 @@ SIGNATURES: dict[str, tuple] = {
     "pidb_gram_reduce": (_int, [_p, _i64, _p, _p, _p, _p]),
     "pidb_depth_epilogue": (_int, [_int, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "pidb_inverse_masses": (_int, [_i64, _p, _p, _p]),
-    "pidb_eid_exact_epilogue": (_int, [_p, _i64, _p, _p, _p, _p, _p]),
+    "pidb_eid_exact_epilogue": (_int, [_p, _i64, _p, _p, _p, _p, _p, _p]),
     "pidb_eid_factorized_epilogue": (
         _int,
         [_i64, _p, _p, _p, _dbl, _p, _p, _p, _p, _p, _p],

@@ -131,7 +131,7 @@ __device__ __forceinline__ uint64_t eid_term_bits53(int64_t m_i, int64_t inter) 
 
 __global__ void eid_exact_kernel(const int64_t* __restrict__ g, int64_t n,
                                  double* __restrict__ in_in, double* __restrict__ in_out,
-                                 double* __restrict__ depth) {
+                                 double* __restrict__ depth, double* __restrict__ mass) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
   for (int64_t i = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5); i < n;
@@ -153,6 +153,7 @@ __global__ void eid_exact_kernel(const int64_t* __restrict__ g, int64_t n,
       col += ((unsigned __int128)ch << 64) | cl;
     }
     if (lane == 0) {
+      if (mass) mass[i] = (double)mi;  // |C_i|, exact
       const double rs = __dmul_rn(u128_to_double_rn(row), 1.1102230246251565e-16);  // 2^-53
       const double cs = __dmul_rn(u128_to_double_rn(col), 1.1102230246251565e-16);
       const double ii = __ddiv_rn(rs, (double)n);
@@ -226,10 +227,10 @@ extern "C" int pidb_gram_reduce(const double* gram, int64_t n, const double* inv
 
 extern "C" int pidb_eid_exact_epilogue(const int64_t* gram, int64_t n, double* in_in,
                                        double* in_out, double* depth, int64_t* rank,
-                                       void* stream) {
+                                       double* mass, void* stream) {
   PIDB_REQUIRE(n >= 1 && gram && in_in && in_out && depth, "bad arguments to pidb_eid_exact_epilogue");
   cudaStream_t st = (cudaStream_t)stream;
-  eid_exact_kernel<<<blocks_for(n, 8), 256, 0, st>>>(gram, n, in_in, in_out, depth);
+  eid_exact_kernel<<<blocks_for(n, 8), 256, 0, st>>>(gram, n, in_in, in_out, depth, mass);
   PIDB_LAUNCH_CHECK("eid_exact_kernel");
   return launch_ranks(n, depth, rank, st);
 }

@@ -327,18 +327,24 @@ def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
     resolve_workers(workers)
     de = stage(ensemble)
     n, dev = de.n, de.device
-    mass, nb = _masses_device(de, with_nonbinary=True)
-    _raise_first_nonbinary(de, nb)
     out = _Out(n, dev)
-    if de.weights is None and N.has_symbol("pidb_gram_i8"):
-        from .reduction import intersection_gram
+    if de.weights is None:
+        from .reduction import intersection_gram, pack_binary
 
-        g = intersection_gram(de)
-        ii, io, d = out.ptrs()[1:]
+        # K7 packs and counts non-binary values in the same pass; the masses
+        # are the Gram diagonal |C_i| (exact integers)
+        nb = torch.zeros(n, dtype=torch.int64, device=dev)
+        packed = pack_binary(de, nb)
+        _allreduce(nb, de)
+        _raise_first_nonbinary(de, nb)
+        g = intersection_gram(de, packed)
+        mslot, ii, io, d = out.ptrs()
         N.call("pidb_eid_exact_epilogue", g.data_ptr(), n, ii, io, d, out.rank.data_ptr(),
-               stream_ptr(dev))
-        masses = mass.cpu().numpy()
+               mslot, stream_ptr(dev))
+        masses = out.vals[:n].cpu().numpy()
     else:
+        mass, nb = _masses_device(de, with_nonbinary=True)
+        _raise_first_nonbinary(de, nb)
         buf = _mean_partials(de)
         p = buf.data_ptr()
         inv = out.ptrs()[0]

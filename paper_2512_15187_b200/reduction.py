@@ -47,19 +47,23 @@ def gram_device(de: DeviceEnsemble) -> torch.Tensor:
     return g
 
 
-def pack_binary(de: DeviceEnsemble) -> torch.Tensor:
-    """K7: 0/1 members -> uint8 rows (row stride a multiple of 128 bytes)."""
+def pack_binary(de: DeviceEnsemble, nonbinary: torch.Tensor | None = None) -> torch.Tensor:
+    """K7: 0/1 members -> uint8 rows (row stride a multiple of 128 bytes);
+    optionally counts each member's values that are neither 0 nor 1
+    (`nonbinary`, int64 (n,) zero-filled by the caller)."""
     ldb = (de.m + 127) // 128 * 128
     b = torch.empty((de.n, ldb), dtype=torch.uint8, device=de.device)
-    N.call("pidb_binary_pack", de.ptr(), de.dtype_code, de.n, de.m, de.ld, b.data_ptr(), ldb,
-           None, stream_ptr(de.device))
+    from .depth import _launch
+
+    _launch("pidb_binary_pack", de.ptr(), de.dtype_code, de.n, de.m, de.ld, b.data_ptr(), ldb,
+            None if nonbinary is None else nonbinary.data_ptr(), stream_ptr(de.device))
     return b
 
 
-def intersection_gram(de: DeviceEnsemble) -> torch.Tensor:
+def intersection_gram(de: DeviceEnsemble, packed: torch.Tensor | None = None) -> torch.Tensor:
     """I[i, j] = |C_i ∩ C_j| exactly (int64), via K7 + K2."""
     lib = N.load()
-    b = pack_binary(de)
+    b = pack_binary(de) if packed is None else packed
     g = torch.empty((de.n, de.n), dtype=torch.int64, device=de.device)
     ws = de.workspace(lib.pidb_gram_i8_workspace_bytes(de.n, de.m))
     from .depth import _launch
