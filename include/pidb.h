@@ -53,7 +53,16 @@ enum pidb_dtype { PIDB_F32 = 0, PIDB_F64 = 1 };
 /* Epilogue modes for pidb_depth_epilogue. */
 enum pidb_epilogue_mode {
   PIDB_EPI_PID_MEAN = 0, /* /root/reference/pkg/src/fuzzdepth/depth.py:274-279 */
-  PIDB_EPI_PID = 1       /* /root/reference/pkg/src/fuzzdepth/depth.py:226-227 */
+  PIDB_EPI_PID = 1,      /* /root/reference/pkg/src/fuzzdepth/depth.py:226-227 */
+  PIDB_EPI_DICE = 2,     /* fuzzy_dice vs the mean mask, depth.py:298-325      */
+  PIDB_EPI_IOU = 3       /* prob_iou vs the mean mask, depth.py:298-325        */
+};
+
+/* Pair operators for pidb_pair_sums. */
+enum pidb_pair_op {
+  PIDB_OP_INCLUSION = 0, /* prob_inclusion, inclusion.py:22-40  */
+  PIDB_OP_SUBSET = 1,    /* subset_epsilon, inclusion.py:43-64  */
+  PIDB_OP_MINMAX = 2     /* _min_max_terms, inclusion.py:67-88  */
 };
 
 int pidb_abi_version(void);
@@ -132,6 +141,7 @@ int pidb_gram_reduce(const double* gram, int64_t n, const double* inv,
  * ranks (stable, descending, ties by index; depth.py:80-85).
  *   mode PID_MEAN: aux = col_mean (1 double), a = row_plain
  *   mode PID     : aux = col_inv  (n doubles), a = row_plain
+ *   mode DICE/IOU: aux = col_mean (1 double), a = sum_min (in_in = in_out)
  * `inv` (n doubles) is written with the inverse masses. */
 int pidb_depth_epilogue(int mode, int64_t n, const double* a,
                         const double* mass, const double* aux, double* inv,
@@ -183,13 +193,27 @@ int pidb_validate(void* u, int dtype, int64_t n, int64_t m, int64_t ld, int clam
                   void* stats, void* stream);
 
 /* ---------------------------------------------------------------- K8 ----
- * prob_inclusion (inclusion.py:22-40): out[0] = sum w u v, out[1] = sum w u.
- * subset_epsilon (inclusion.py:43-64) on 0/1 data: out[0] = sum w a (1-b),
- * out[1] = sum w a.  Additive over cell shards.  Synchronous (returns after
- * the sums are in `out`, a HOST pointer to 2 doubles). */
+ * Pair sums, one fused pass (synchronous: returns after the sums are in
+ * `out_host`, a HOST pointer to 2 doubles, 4 for PIDB_OP_MINMAX):
+ *   PIDB_OP_INCLUSION: {sum w u v, sum w u}       (prob_inclusion)
+ *   PIDB_OP_SUBSET   : {sum w a (1-b), sum w a}   (subset_epsilon, 0/1 data)
+ *   PIDB_OP_MINMAX   : {sum w min(u,v), sum w max(u,v), sum w u, sum w v}
+ *                      (fuzzy_dice / prob_iou, inclusion.py:67-107)
+ * Workspace: (4 * min(592, ceil(m/256)) + 4) doubles. */
 int pidb_pair_sums(const void* u, const void* v, int dtype, int64_t m,
-                   const double* w, int complement, double* out_host,
+                   const double* w, int op, double* out_host,
                    void* ws, size_t ws_bytes, void* stream);
+
+/* Similarity-baseline partials in one pass (depth_similarity_baseline,
+ * depth.py:298-325, against the mean mask):
+ *   sum_min[i] = sum_x w min(u_i, mean), mass[i] = sum_x w u_i,
+ *   col_mean[0] = sum_x w S(x) (= n * mask_mass(mean)); with
+ *   sum w max(u_i, mean) = mass_i + col_mean/n - sum_min_i.
+ * Same workspace as pidb_pid_mean_partials. */
+int pidb_similarity_partials(const void* u, int dtype, int64_t n, int64_t m,
+                             int64_t ld, const double* w, double* sum_min,
+                             double* mass, double* col_mean, void* ws,
+                             size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- synth --
  * Device-side synthetic ensembles (benchmark/test infrastructure; the

@@ -210,3 +210,47 @@ def subset_epsilon(a, b, w=None) -> float:
             excess += float(np.count_nonzero(out))
             mass += float(np.count_nonzero(ac))
     return 0.0 if mass == 0.0 else 1.0 - excess / mass
+
+
+def min_max_terms(u, v, w=None):
+    """_min_max_terms (inclusion.py:67-88)."""
+    s_min = s_max = s_u = s_v = 0.0
+    for lo, hi in _spans(u.shape[0]):
+        uc = u[lo:hi].astype(np.float64, copy=False)
+        vc = v[lo:hi].astype(np.float64, copy=False)
+        lo_uv, hi_uv = np.minimum(uc, vc), np.maximum(uc, vc)
+        if w is not None:
+            wc = w[lo:hi]
+            lo_uv, hi_uv, uc, vc = wc * lo_uv, wc * hi_uv, wc * uc, wc * vc
+        s_min += float(np.sum(lo_uv))
+        s_max += float(np.sum(hi_uv))
+        s_u += float(np.sum(uc))
+        s_v += float(np.sum(vc))
+    return s_min, s_max, s_u, s_v
+
+
+def fuzzy_dice(u, v, w=None) -> float:
+    """inclusion.py:91-96; ValueError for two zero-mass masks."""
+    s_min, _, s_u, s_v = min_max_terms(u, v, w)
+    if s_u + s_v == 0.0:
+        raise ValueError("fuzzy_dice is undefined for two zero-mass masks")
+    return 2.0 * s_min / (s_u + s_v)
+
+
+def prob_iou(u, v, w=None) -> float:
+    """inclusion.py:99-107; ValueError for two zero-mass masks."""
+    s_min, s_max, _, _ = min_max_terms(u, v, w)
+    if s_max == 0.0:
+        raise ValueError("prob_iou is undefined for two zero-mass masks")
+    return s_min / s_max
+
+
+def depth_similarity(U, measure, w=None, workers=None):
+    """depth_similarity_baseline (depth.py:298-325): similarity to the mean mask."""
+    fn = {"dice": fuzzy_dice, "fuzzy-dice": fuzzy_dice, "iou": prob_iou, "prob-iou": prob_iou}[measure]
+    mean = mean_values(U)
+    if weighted_sum(mean, w) == 0.0:
+        raise ValueError("ensemble mean mask is identically zero")
+    m_ = masses(U, w, workers)
+    d = np.array(_pmap(lambda i: fn(U[i], mean, w), range(len(U)), _workers(workers)))
+    return _pack(d, d.copy(), m_)

@@ -12,10 +12,12 @@ from .depth import (
     METHOD_NAMES,
     TILE_BYTES,
     DepthResult,
+    compare_pid_vs_mean,
     depth_by_method,
     depth_eid,
     depth_pid,
     depth_pid_mean,
+    depth_similarity_baseline,
     mass_cv,
     member_masses,
     ranks_from_depths,
@@ -42,7 +44,7 @@ from .grid import (
     mean_mask,
     permute_cells,
 )
-from .inclusion import prob_inclusion, subset_epsilon
+from .inclusion import fuzzy_dice, prob_inclusion, prob_iou, subset_epsilon
 from .reduction import gram_block
 
 __version__ = "0.1.0"
@@ -66,10 +68,13 @@ __all__ = [
     "binarize",
     "binarize_ensemble",
     "binary_mass",
+    "compare_pid_vs_mean",
     "depth_by_method",
     "depth_eid",
     "depth_pid",
     "depth_pid_mean",
+    "depth_similarity_baseline",
+    "fuzzy_dice",
     "gram_block",
     "mask_mass",
     "mass_cv",
@@ -77,6 +82,7 @@ __all__ = [
     "member_masses",
     "permute_cells",
     "prob_inclusion",
+    "prob_iou",
     "ranks_from_depths",
     "resolve_workers",
     "shard_bounds",

@@ -25,6 +25,11 @@ PIDB_F32 = 0
 PIDB_F64 = 1
 PIDB_EPI_PID_MEAN = 0
 PIDB_EPI_PID = 1
+PIDB_EPI_DICE = 2
+PIDB_EPI_IOU = 3
+PIDB_OP_INCLUSION = 0
+PIDB_OP_SUBSET = 1
+PIDB_OP_MINMAX = 2
 
 
 class NativeError(RuntimeError):
@@ -43,6 +48,7 @@ SIGNATURES: dict[str, tuple] = {
     "pidb_last_error": (C.c_char_p, []),
     "pidb_pid_mean_workspace_bytes": (_sz, [_i64, _i64, _int]),
     "pidb_pid_mean_partials": (_int, [_p, _int, _i64, _i64, _i64, _p, _p, _p, _p, _p, _sz, _p]),
+    "pidb_similarity_partials": (_int, [_p, _int, _i64, _i64, _i64, _p, _p, _p, _p, _p, _sz, _p]),
     "pidb_pid_colsums": (_int, [_p, _int, _i64, _i64, _i64, _p, _p, _p, _p, _sz, _p]),
     "pidb_member_masses": (_int, [_p, _int, _i64, _i64, _i64, _p, _p, _p, _p, _sz, _p]),
     "pidb_binary_pack": (_int, [_p, _int, _i64, _i64, _i64, _p, _i64, _p, _p]),

@@ -56,38 +56,52 @@ __global__ void binary_pack_kernel(const T* __restrict__ u, int64_t n, int64_t m
 }
 
 // ------------------------------------------------------------------ K8 ------
+// op 0 (prob_inclusion):  [sum w u v, sum w u]
+// op 1 (subset_epsilon):  [sum w a (b == 0), sum w a]
+// op 2 (_min_max_terms, inclusion.py:67-88): [sum w min, sum w max, sum w u, sum w v]
 template <typename T>
 __global__ void pair_sums_kernel(const T* __restrict__ u, const T* __restrict__ v, int64_t m,
-                                 const double* __restrict__ w, int complement,
+                                 const double* __restrict__ w, int op,
                                  double* __restrict__ part) {
-  double num = 0.0, den = 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m;
        x += (int64_t)gridDim.x * blockDim.x) {
-    double a = (double)u[x];
+    const double a = (double)u[x];
     const double bv = (double)v[x];
-    if (w) a *= w[x];
-    num = fma(a, complement ? (bv != 0.0 ? 0.0 : 1.0) : bv, num);
-    den += a;
+    const double wx = w ? w[x] : 1.0;
+    if (op == 2) {
+      acc[0] = fma(wx, fmin(a, bv), acc[0]);
+      acc[1] = fma(wx, fmax(a, bv), acc[1]);
+      acc[2] = fma(wx, a, acc[2]);
+      acc[3] = fma(wx, bv, acc[3]);
+    } else {
+      const double wa = a * wx;
+      acc[0] = fma(wa, op == 1 ? (bv != 0.0 ? 0.0 : 1.0) : bv, acc[0]);
+      acc[1] += wa;
+    }
   }
-  __shared__ double s[2][32];
-  num = warp_sum(num);
-  den = warp_sum(den);
-  if ((threadIdx.x & 31) == 0) { s[0][threadIdx.x >> 5] = num; s[1][threadIdx.x >> 5] = den; }
+  __shared__ double s[4][32];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double t = warp_sum(acc[q]);
+    if ((threadIdx.x & 31) == 0) s[q][threadIdx.x >> 5] = t;
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int k = 0; k < (int)(blockDim.x / 32); ++k) { a += s[0][k]; b += s[1][k]; }
-    part[2 * blockIdx.x] = a;
-    part[2 * blockIdx.x + 1] = b;
+  if (threadIdx.x < 4) {
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x / 32); ++k) t += s[threadIdx.x][k];
+    part[4 * blockIdx.x + threadIdx.x] = t;
   }
 }
 
 __global__ void pair_finish_kernel(const double* __restrict__ part, int nb, double* out) {
-  double a = 0.0, b = 0.0;
-  for (int k = threadIdx.x; k < nb; k += 32) { a += part[2 * k]; b += part[2 * k + 1]; }
-  a = warp_sum(a);
-  b = warp_sum(b);
-  if (threadIdx.x == 0) { out[0] = a; out[1] = b; }
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k = threadIdx.x; k < nb; k += 32)
+    for (int q = 0; q < 4; ++q) a[q] += part[4 * k + q];
+  for (int q = 0; q < 4; ++q) {
+    const double t = warp_sum(a[q]);
+    if (threadIdx.x == 0) out[q] = t;
+  }
 }
 
 // ---------------------------------------------------------------- synth -----
@@ -174,27 +188,27 @@ extern "C" int pidb_binary_pack(const void* u, int dtype, int64_t n, int64_t m, 
 }
 
 extern "C" int pidb_pair_sums(const void* u, const void* v, int dtype, int64_t m, const double* w,
-                              int complement, double* out_host, void* ws, size_t ws_bytes,
+                              int op, double* out_host, void* ws, size_t ws_bytes,
                               void* stream) {
   PIDB_REQUIRE(u && v && out_host && m >= 1, "bad arguments to pidb_pair_sums");
+  PIDB_REQUIRE(op >= PIDB_OP_INCLUSION && op <= PIDB_OP_MINMAX, "unknown pair op %d", op);
   const int nb = (int)std::min<int64_t>(4 * 148, (m + 255) / 256);
-  PIDB_REQUIRE(ws && ws_bytes >= (size_t)(2 * nb + 2) * sizeof(double),
+  PIDB_REQUIRE(ws && ws_bytes >= (size_t)(4 * nb + 4) * sizeof(double),
                "workspace too small for pidb_pair_sums (need %zu bytes)",
-               (size_t)(2 * nb + 2) * sizeof(double));
+               (size_t)(4 * nb + 4) * sizeof(double));
   cudaStream_t st = (cudaStream_t)stream;
   double* part = static_cast<double*>(ws);
   if (dtype == PIDB_F32)
     pair_sums_kernel<float><<<nb, 256, 0, st>>>(static_cast<const float*>(u),
-                                                static_cast<const float*>(v), m, w, complement,
-                                                part);
+                                                static_cast<const float*>(v), m, w, op, part);
   else
     pair_sums_kernel<double><<<nb, 256, 0, st>>>(static_cast<const double*>(u),
-                                                 static_cast<const double*>(v), m, w, complement,
-                                                 part);
+                                                 static_cast<const double*>(v), m, w, op, part);
   PIDB_LAUNCH_CHECK("pair_sums_kernel");
-  pair_finish_kernel<<<1, 32, 0, st>>>(part, nb, part + 2 * nb);
+  pair_finish_kernel<<<1, 32, 0, st>>>(part, nb, part + 4 * nb);
   PIDB_LAUNCH_CHECK("pair_finish_kernel");
-  PIDB_CUDA(cudaMemcpyAsync(out_host, part + 2 * nb, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  const int nout = op == PIDB_OP_MINMAX ? 4 : 2;
+  PIDB_CUDA(cudaMemcpyAsync(out_host, part + 4 * nb, nout * sizeof(double), cudaMemcpyDeviceToHost, st));
   PIDB_CUDA(cudaStreamSynchronize(st));
   return PIDB_OK;
 }

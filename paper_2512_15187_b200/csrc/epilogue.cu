@@ -22,6 +22,9 @@ __global__ void inverse_masses_kernel(int64_t n, const double* __restrict__ mass
   }
 }
 
+// Internal mode (not in the public enum): binary weighted eID.
+constexpr int kEpiEidFact = 100;
+
 // mode PID_MEAN: a=row_plain (= N*num), aux[0] = col_mean (= N*mean_mass_total)
 // mode PID     : a=row_plain, aux = col_inv
 // mode EID_FACT: a=row_plain, aux = col_inv (binary weighted eID via the
@@ -46,7 +49,14 @@ __global__ void depth_values_kernel(int mode, int64_t n, const double* __restric
     } else if (mode == PIDB_EPI_PID) {
       ii = __ddiv_rn(__dmul_rn(iv, a[i]), dn);
       io = __ddiv_rn(aux[i], dn);
-    } else {
+    } else if (mode == PIDB_EPI_DICE || mode == PIDB_EPI_IOU) {
+      // a = sum w min(u_i, mean), aux[0] = n * mean mass; max = u + mean - min
+      const double s_v = __ddiv_rn(aux[0], dn);
+      const double den = mode == PIDB_EPI_DICE ? __dadd_rn(mi, s_v)
+                                               : __dsub_rn(__dadd_rn(mi, s_v), a[i]);
+      ii = mode == PIDB_EPI_DICE ? __ddiv_rn(__dmul_rn(2.0, a[i]), den) : __ddiv_rn(a[i], den);
+      io = ii;
+    } else {  // kEpiEidFact
       const double row_excess = __dsub_rn(__dmul_rn(dn, mi), a[i]);
       const double col_excess = __dsub_rn(n_pos, aux[i]);
       ii = mi > 0.0 ? __ddiv_rn(__dsub_rn(dn, __dmul_rn(iv, row_excess)), dn) : 0.0;
@@ -194,7 +204,7 @@ extern "C" int pidb_depth_epilogue(int mode, int64_t n, const double* a, const d
                                    double* in_out, double* depth, int64_t* rank, void* stream) {
   PIDB_REQUIRE(n >= 1, "n must be >= 1");
   PIDB_REQUIRE(a && mass && aux && inv && in_in && in_out && depth, "NULL epilogue pointer");
-  PIDB_REQUIRE(mode == PIDB_EPI_PID_MEAN || mode == PIDB_EPI_PID, "unknown epilogue mode %d", mode);
+  PIDB_REQUIRE(mode >= PIDB_EPI_PID_MEAN && mode <= PIDB_EPI_IOU, "unknown epilogue mode %d", mode);
   cudaStream_t st = (cudaStream_t)stream;
   depth_values_kernel<<<blocks_for(n, 256), 256, 0, st>>>(mode, n, a, mass, aux, inv, in_in,
                                                           in_out, depth, 0.0);
@@ -210,7 +220,7 @@ extern "C" int pidb_eid_factorized_epilogue(int64_t n, const double* row_plain,
   PIDB_REQUIRE(n >= 1 && row_plain && mass && col_inv && inv && in_in && in_out && depth,
                "bad arguments to pidb_eid_factorized_epilogue");
   cudaStream_t st = (cudaStream_t)stream;
-  depth_values_kernel<<<blocks_for(n, 256), 256, 0, st>>>(2, n, row_plain, mass, col_inv, inv,
+  depth_values_kernel<<<blocks_for(n, 256), 256, 0, st>>>(kEpiEidFact, n, row_plain, mass, col_inv, inv,
                                                           in_in, in_out, depth, n_pos);
   PIDB_LAUNCH_CHECK("depth_values_kernel");
   return launch_ranks(n, depth, rank, st);

@@ -44,6 +44,7 @@ constexpr int kPhases = kThreads / kChunks16;  // row phases of the column sweep
 constexpr int MODE_MEAN = 0;
 constexpr int MODE_COLS = 1;
 constexpr int MODE_MASS = 2;  // masses (+ non-binary count): row sweep only
+constexpr int MODE_SIM = 3;   // similarity baselines: sum w*min(u, mean), masses
 
 struct StreamParams {
   int64_t n, m, tiles;
@@ -189,7 +190,7 @@ __device__ __forceinline__ void finish_partials(const StreamParams& p, int pncb,
       }
     }
   }
-  if (warp == 0 && p.mode == MODE_MEAN) {
+  if (warp == 0 && (p.mode == MODE_MEAN || p.mode == MODE_SIM)) {
     double c = 0.0;
     for (int g = lane; g < G; g += 32) c += __ldcg(p.part_col + g);
     c = warp_sum(c);
@@ -219,7 +220,8 @@ __device__ __forceinline__ void finalize_tile(const StreamParams& p, const doubl
       double S = 0.0;
 #pragma unroll
       for (int k = 0; k < kWarps; ++k) S += rd[k * V + v];
-      sS[slot] = wx * S;
+      // MODE_SIM keeps the mean mask value (mean_mask, grid.py:251-261)
+      sS[slot] = p.mode == MODE_SIM ? __ddiv_rn(S, (double)p.n) : wx * S;
       col_acc = fma(wx, S, col_acc);
     }
   }
@@ -249,6 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n = (int)p.n;
   const int G = gridDim.x;
   const int mode = p.mode;
+  const int sweep = mode == MODE_SIM ? MODE_MEAN : mode;  // pass-1 column kind
   const bool weighted = p.w != nullptr;
   const int64_t my_tiles = p.tiles > blockIdx.x ? (p.tiles - 1 - blockIdx.x) / G + 1 : 0;
   const uint64_t pol = policy_evict_first();
@@ -304,6 +307,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
     if (mode == MODE_MEAN && !weighted) {
       PIDB_ROWS_LOOP(acc_row[k] = fma(v[e], s_l[e], acc_row[k]); acc_mass[k] += v[e])
+    } else if (mode == MODE_SIM) {
+      PIDB_ROWS_LOOP(acc_row[k] = fma(fmin(v[e], s_l[e]), w_l[e], acc_row[k]);
+                     acc_mass[k] = fma(v[e], w_l[e], acc_mass[k]))
     } else if (mode == MODE_MASS) {
       PIDB_ROWS_LOOP(acc_mass[k] = fma(v[e], w_l[e], acc_mass[k]); acc_nb[k] += is_nonbinary(v[e]))
     } else if (mode == MODE_COLS) {
@@ -325,8 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&full[s_cur], par);
       if (mode != MODE_MASS) {
         cs.reset();
-        cs.run(tiles + (size_t)s_cur * p.stage_bytes + p1_off, ph, n, mode, p.inv, ph, n);
-        cs.combine(mode);
+        cs.run(tiles + (size_t)s_cur * p.stage_bytes + p1_off, ph, n, sweep, p.inv, ph, n);
+        cs.combine(sweep);
         if (lane < 16) {
 #pragma unroll
           for (int e = 0; e < EPC; ++e) rd[warp * V + q * EPC + e] = cs.part[e];
@@ -396,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int G = gridDim.x;
   const int C = (n + kChunkRows - 1) / kChunkRows;
   const int mode = p.mode;
+  const int sweep = mode == MODE_SIM ? MODE_MEAN : mode;  // pass-1 column kind
   const bool two_touch = mode != MODE_MASS;
   const int loads_per_tile = two_touch ? 2 * C : C;
   const bool weighted = p.w != nullptr;
@@ -454,10 +461,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       cs.reset();
       for (int c = 0; c < C; ++c) {
         const unsigned char* st = next_chunk();
-        cs.run(st + a_off, ph, kChunkRows, mode, p.inv, c * kChunkRows + ph, n);
+        cs.run(st + a_off, ph, kChunkRows, sweep, p.inv, c * kChunkRows + ph, n);
         release_chunk();
       }
-      cs.combine(mode);
+      cs.combine(sweep);
       if (lane < 16) {
 #pragma unroll
         for (int e = 0; e < EPC; ++e) red[warp * V + q * EPC + e] = cs.part[e];
@@ -489,6 +496,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int e = 0; e < EPC; ++e) {
                 am[e] = fma(v[e], W[e * 8 + Lr], am[e]);
                 nb += is_nonbinary(v[e]);
+              }
+            } else if (mode == MODE_SIM) {
+#pragma unroll
+              for (int e = 0; e < EPC; ++e) {
+                ar[e] = fma(fmin(v[e], S[e * 8 + Lr]), W[e * 8 + Lr], ar[e]);
+                am[e] = fma(v[e], W[e * 8 + Lr], am[e]);
               }
             } else if (mode == MODE_COLS) {
 #pragma unroll
@@ -701,6 +714,15 @@ extern "C" int pidb_pid_mean_partials(const void* u, int dtype, int64_t n, int64
                                       double* col_mean, void* ws, size_t ws_bytes, void* stream) {
   PIDB_REQUIRE(row_plain && mass && col_mean, "output pointers must be non-NULL");
   return pidb::run_stream_pass(pidb::MODE_MEAN, u, dtype, n, m, ld, w, nullptr, row_plain, mass,
+                               col_mean, nullptr, ws, ws_bytes, stream);
+}
+
+extern "C" int pidb_similarity_partials(const void* u, int dtype, int64_t n, int64_t m,
+                                        int64_t ld, const double* w, double* sum_min,
+                                        double* mass, double* col_mean, void* ws,
+                                        size_t ws_bytes, void* stream) {
+  PIDB_REQUIRE(sum_min && mass && col_mean, "output pointers must be non-NULL");
+  return pidb::run_stream_pass(pidb::MODE_SIM, u, dtype, n, m, ld, w, nullptr, sum_min, mass,
                                col_mean, nullptr, ws, ws_bytes, stream);
 }
 

@@ -358,6 +358,68 @@ def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
     return _finish(de, out, "eid", masses, t0)
 
 
+_BASELINES = {"dice": "dice", "fuzzy-dice": "dice", "iou": "iou", "prob-iou": "iou"}
+
+
+def depth_similarity_baseline(ensemble, measure: str, workers: int | None = None) -> DepthResult:
+    """Depth as the symmetric similarity of each member to the mean mask
+    (depth.py:298-325): fuzzy Dice or probabilistic IoU.  One device pass
+    forms sum w*min(u_i, mean) and the masses (sum w*max follows from
+    min + max = u + mean)."""
+    try:
+        kind = _BASELINES[measure]
+    except KeyError:
+        raise ValidationError(
+            f"unknown similarity measure {measure!r}; expected one of {sorted(_BASELINES)}"
+        ) from None
+    t0 = time.perf_counter()
+    resolve_workers(workers)
+    de = stage(ensemble)
+    n, dev = de.n, de.device
+    buf = _f64(2 * n + 1, dev)
+    ws = de.workspace(N.load().pidb_pid_mean_workspace_bytes(de.n, de.m, de.dtype_code))
+    p = buf.data_ptr()
+    _launch("pidb_similarity_partials", de.ptr(), de.dtype_code, n, de.m, de.ld, de.wptr(),
+            p, p + 8 * n, p + 16 * n, ws.data_ptr(), ws.numel(), stream_ptr(dev))
+    _allreduce(buf, de)
+    out = _Out(n, dev)
+    inv, ii, io, d = out.ptrs()
+    N.call("pidb_depth_epilogue", N.PIDB_EPI_DICE if kind == "dice" else N.PIDB_EPI_IOU, n,
+           p, p + 8 * n, p + 16 * n, inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
+    host = buf[n:].cpu().numpy()
+    if float(host[n]) == 0.0:
+        raise DegenerateEnsembleError("ensemble mean mask is identically zero")
+    return _finish(de, out, kind, host[:n], t0)
+
+
+def compare_pid_vs_mean(ensemble, workers: int | None = None) -> dict:
+    """Exact PID vs PID-mean: depth error and rank agreement (depth.py:328-346)."""
+    from scipy import stats
+
+    de = stage(ensemble)
+    if de.n < 2:
+        raise ValidationError("comparison needs at least two members")
+    exact = depth_pid(de, workers)
+    approx = depth_pid_mean(de, workers)
+    err = np.abs(exact.depth - approx.depth)
+
+    def _pearson(x, y):
+        dx = np.asarray(x, dtype=np.float64) - np.mean(x)
+        dy = np.asarray(y, dtype=np.float64) - np.mean(y)
+        sx, sy = float(np.sum(dx * dx)), float(np.sum(dy * dy))
+        if sx == 0.0 or sy == 0.0:
+            raise ValidationError("pearson undefined: an input has zero variance")
+        return float(np.sum(dx * dy) / np.sqrt(sx * sy))
+
+    return {
+        "max_abs_error": float(err.max()),
+        "mean_abs_error": float(err.mean()),
+        "rank_pearson": _pearson(exact.rank, approx.rank),
+        "rank_kendall": float(stats.kendalltau(exact.rank, approx.rank, variant="b").statistic),
+        "cv_mass": approx.cv_mass,
+    }
+
+
 def depth_by_method(ensemble, method: str, workers: int | None = None) -> DepthResult:
     """Dispatch on a method name (depth.py:349-363)."""
     if method == "eid":
@@ -366,9 +428,6 @@ def depth_by_method(ensemble, method: str, workers: int | None = None) -> DepthR
         return depth_pid(ensemble, workers)
     if method == "pid-mean":
         return depth_pid_mean(ensemble, workers)
-    if method in ("dice", "iou", "fuzzy-dice", "prob-iou"):
-        raise ValidationError(
-            f"method {method!r} (similarity baseline, depth.py:290-325) is outside the "
-            "B200 hot path; use fuzzdepth.depth_similarity_baseline"
-        )
+    if method in _BASELINES:
+        return depth_similarity_baseline(ensemble, method, workers)
     raise ValidationError(f"unknown depth method {method!r}; expected one of {METHOD_NAMES}")

@@ -205,7 +205,7 @@ def _weights(weights, m, dev, lo: int = 0, hi: int | None = None):
         raise ValidationError(f"weights shape {w_host.shape} does not match cell count {m}")
     if not np.isfinite(w_host).all() or (w_host <= 0).any():
         raise ValidationError("cell weights must be finite and positive")
-    w_dev = torch.from_numpy(np.ascontiguousarray(w_host[lo:hi])).to(dev)
+    w_dev = torch.tensor(w_host[lo:hi], dtype=torch.float64, device=dev)
     return w_host, w_dev
 
 

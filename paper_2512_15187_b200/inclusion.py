@@ -1,5 +1,6 @@
-"""Pairwise operators on the GPU (K8): probabilistic inclusion and the binary
-epsilon-subset, /root/reference/pkg/src/fuzzdepth/inclusion.py:22-64.
+"""Pairwise operators on the GPU (K8): probabilistic inclusion, the binary
+epsilon-subset and the symmetric Dice / IoU similarities,
+/root/reference/pkg/src/fuzzdepth/inclusion.py:22-107.
 
 Both take one fused pass over the cells (numerator and denominator together)
 with fp64 accumulation, like the reference.  Inputs are the reference's mask
@@ -13,6 +14,7 @@ import torch
 
 from . import _native as N
 from .device import require_cuda, stream_ptr
+from .errors import ValidationError
 
 _WS: dict = {}
 
@@ -29,7 +31,7 @@ def _dev_values(x, dev, dtype=None) -> torch.Tensor:
     return t.to(dev).contiguous()
 
 
-def _pair(u_vals, v_vals, weights, complement: bool) -> tuple[float, float]:
+def _pair(u_vals, v_vals, weights, op: int) -> tuple[float, ...]:
     dev = require_cuda()
     dt = torch.float64 if (getattr(u_vals, "dtype", None) in (np.float64, torch.float64) or
                            getattr(v_vals, "dtype", None) in (np.float64, torch.float64)) else torch.float32
@@ -41,18 +43,18 @@ def _pair(u_vals, v_vals, weights, complement: bool) -> tuple[float, float]:
     ws = _WS.get(key)
     if ws is None:
         ws = _WS[key] = torch.empty(8192 * 8, dtype=torch.uint8, device=dev)
-    out = np.zeros(2, dtype=np.float64)
+    out = np.zeros(4, dtype=np.float64)
     N.call("pidb_pair_sums", u.data_ptr(), v.data_ptr(),
            N.PIDB_F64 if dt == torch.float64 else N.PIDB_F32, m,
-           None if w is None else w.data_ptr(), int(complement),
+           None if w is None else w.data_ptr(), int(op),
            out.ctypes.data, ws.data_ptr(), ws.numel(), stream_ptr(dev))
-    return float(out[0]), float(out[1])
+    return tuple(float(x) for x in out[:4 if op == N.PIDB_OP_MINMAX else 2])
 
 
 def prob_inclusion(u, v) -> float:
     """(sum w u v) / (sum w u); 0 when u has zero mass (inclusion.py:22-40)."""
     u.grid.require_same(v.grid)
-    num, den = _pair(u.values, v.values, u.grid.weights, complement=False)
+    num, den = _pair(u.values, v.values, u.grid.weights, N.PIDB_OP_INCLUSION)
     if den == 0.0:
         return 0.0
     return num / den
@@ -63,7 +65,29 @@ def subset_epsilon(a, b) -> float:
     a.grid.require_same(b.grid)
     av = np.asarray(a.bits, dtype=np.float32)
     bv = np.asarray(b.bits, dtype=np.float32)
-    excess, mass = _pair(av, bv, a.grid.weights, complement=True)
+    excess, mass = _pair(av, bv, a.grid.weights, N.PIDB_OP_SUBSET)
     if mass == 0.0:
         return 0.0
     return 1.0 - excess / mass
+
+
+def _min_max_terms(u, v) -> tuple[float, float, float, float]:
+    """Fused sums of w*min(u,v), w*max(u,v), w*u, w*v (inclusion.py:67-88)."""
+    u.grid.require_same(v.grid)
+    return _pair(u.values, v.values, u.grid.weights, N.PIDB_OP_MINMAX)
+
+
+def fuzzy_dice(u, v) -> float:
+    """2 sum(w min(u,v)) / (sum(w u) + sum(w v)) (inclusion.py:91-96)."""
+    s_min, _, s_u, s_v = _min_max_terms(u, v)
+    if s_u + s_v == 0.0:
+        raise ValidationError("fuzzy_dice is undefined for two zero-mass masks")
+    return 2.0 * s_min / (s_u + s_v)
+
+
+def prob_iou(u, v) -> float:
+    """sum(w min(u,v)) / sum(w max(u,v)) (inclusion.py:99-107)."""
+    s_min, s_max, _, _ = _min_max_terms(u, v)
+    if s_max == 0.0:
+        raise ValidationError("prob_iou is undefined for two zero-mass masks")
+    return s_min / s_max

@@ -64,6 +64,9 @@ def result_arrays(prefix, r):
     }
 
 
+CMP_KEYS = ("max_abs_error", "mean_abs_error", "rank_pearson", "rank_kendall", "cv_mass")
+
+
 def save(name, **arrays):
     np.savez_compressed(OUT / f"{name}.npz", **arrays)
     print(name, {k: v.shape for k, v in arrays.items()})
@@ -87,6 +90,11 @@ def main():
             arr["w"] = w
         arr.update(result_arrays("pid", fd.depth_pid(e)))
         arr.update(result_arrays("pidmean", fd.depth_pid_mean(e)))
+        arr.update(result_arrays("dice", fd.depth_similarity_baseline(e, "dice")))
+        arr.update(result_arrays("iou", fd.depth_similarity_baseline(e, "iou")))
+        if n >= 2:
+            cmp = fd.compare_pid_vs_mean(e)
+            arr["cmp"] = np.array([cmp[k] for k in CMP_KEYS])
         arr["mass"] = fd.member_masses(e)
         arr["mean"] = fd.mean_mask(e).values
         if int(np.prod(dims)) * n <= 4000:
@@ -147,7 +155,15 @@ def main():
         w = ws[k] if k % 2 else None
         g = fd.GridSpec((50,), w)
         sub.append(fd.subset_epsilon(fd.BinaryMask(g, a[k]), fd.BinaryMask(g, b[k])))
-    save("pairs", u=us, v=vs, w=ws, inc=np.array(inc), a=a, b=b, sub=np.array(sub))
+    dice, iou = [], []
+    for k in range(6):
+        w = ws[k] if k % 2 else None
+        g = fd.GridSpec((50,), w)
+        pu, pv = fd.ProbMask(g, us[k]), fd.ProbMask(g, vs[k])
+        dice.append(fd.fuzzy_dice(pu, pv))
+        iou.append(fd.prob_iou(pu, pv))
+    save("pairs", u=us, v=vs, w=ws, inc=np.array(inc), a=a, b=b, sub=np.array(sub),
+         dice=np.array(dice), iou=np.array(iou))
 
 
 if __name__ == "__main__":

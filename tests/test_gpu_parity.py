@@ -170,6 +170,51 @@ def test_pairs_golden(pb):
             pytest.approx(z["sub"][k], abs=1e-14)
 
 
+def test_pairs_similarity_golden(pb):
+    z = golden("pairs")
+    for k in range(6):
+        w = z["w"][k] if k % 2 else None
+        g = pb.GridSpec((50,), w)
+        u, v = pb.ProbMask(g, z["u"][k]), pb.ProbMask(g, z["v"][k])
+        assert pb.fuzzy_dice(u, v) == pytest.approx(z["dice"][k], abs=1e-14)
+        assert pb.prob_iou(u, v) == pytest.approx(z["iou"][k], abs=1e-14)
+
+
+@pytest.mark.parametrize("name", golden_names("fuzzy_"))
+def test_similarity_baselines_golden(pb, name):
+    z = golden(name)
+    e = ens(pb, z["U"], z.get("w"), dims=z["dims"])
+    for measure, alias in (("dice", "fuzzy-dice"), ("iou", "prob-iou")):
+        for meth in (measure, alias):
+            r = pb.depth_by_method(e, meth)
+            for k in ("in_in", "in_out", "depth"):
+                close(getattr(r, k), z[f"{measure}_{k}"], 1e-13)
+            np.testing.assert_array_equal(r.rank, z[f"{measure}_rank"])
+            assert r.method == measure
+            assert r.cv_mass == pytest.approx(float(z[f"{measure}_cv"]), abs=1e-12)
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names("fuzzy_") if "cmp" in golden(n)])
+def test_compare_pid_vs_mean_golden(pb, name):
+    z = golden(name)
+    e = ens(pb, z["U"], z.get("w"), dims=z["dims"])
+    rep = pb.compare_pid_vs_mean(e)
+    got = [rep[k] for k in ("max_abs_error", "mean_abs_error", "rank_pearson", "rank_kendall", "cv_mass")]
+    close(got, z["cmp"], 1e-12)
+
+
+@pytest.mark.parametrize("n,dims,weighted", [(5, (37,), False), (300, (40, 40), True),
+                                             (1500, (24, 24), False)])
+def test_similarity_baselines_vs_oracle(pb, n, dims, weighted):
+    U, w = make_fuzzy(2000 + n, n, dims, weighted)
+    e = ens(pb, U, w, dims=dims)
+    for measure in ("dice", "iou"):
+        ref = port.depth_similarity(U, measure, w, workers=8)
+        r = pb.depth_similarity_baseline(e, measure)
+        close(r.depth, ref["depth"], 1e-12)
+        np.testing.assert_array_equal(r.rank, ref["rank"])
+
+
 @pytest.mark.parametrize("name", ["gen_disks", "gen_ellipsoids"])
 def test_generator_fixtures(pb, name):
     z = golden(name)
@@ -215,8 +260,44 @@ def test_trio(pb):
     close(r.depth, [2 / 3, 5 / 6, 0.5], 1e-15)
     assert r.cv_mass == pytest.approx(math.sqrt(2 / 3) / 2, abs=1e-12)
     np.testing.assert_array_equal(pb.member_masses(e), [3.0, 2.0, 1.0])
-    for method in ("eid", "pid", "pid-mean"):
+    for method in ("eid", "pid", "pid-mean", "dice", "iou"):
         assert pb.depth_by_method(e, method).method == method
+    # test_depth.py:233-256
+    r = pb.depth_similarity_baseline(e, "dice")
+    close(r.depth, [0.8, 5 / 6, 2 / 3], 1e-15)
+    np.testing.assert_array_equal(r.rank, [1, 0, 2])
+    close(pb.depth_similarity_baseline(e, "iou").depth, [2 / 3, 5 / 7, 0.5], 1e-15)
+    with pytest.raises(pb.ValidationError):
+        pb.depth_similarity_baseline(e, "hausdorff")
+    rep = pb.compare_pid_vs_mean(e)
+    assert rep["max_abs_error"] == pytest.approx(1 / 9, abs=1e-14)
+    assert rep["mean_abs_error"] == pytest.approx(1 / 27, abs=1e-14)
+    assert rep["rank_pearson"] == pytest.approx(1.0, abs=1e-12)
+    assert rep["rank_kendall"] == pytest.approx(1.0, abs=1e-12)
+
+
+def test_overlap_scores_hand_values(pb):
+    g = pb.GridSpec((4,))
+    u, v = pb.ProbMask(g, [1, 0.5, 0, 0]), pb.ProbMask(g, [0.5, 0.5, 0, 0])
+    assert pb.fuzzy_dice(u, v) == pytest.approx(0.8, abs=1e-15)
+    assert pb.prob_iou(u, v) == pytest.approx(2 / 3, abs=1e-15)
+    a, b = pb.ProbMask(g, [1, 1, 0, 0]), pb.ProbMask(g, [0, 1, 1, 0])
+    assert pb.fuzzy_dice(a, b) == pytest.approx(0.5, abs=1e-15)
+    assert pb.prob_iou(a, b) == pytest.approx(1 / 3, abs=1e-15)
+    z = pb.ProbMask(pb.GridSpec((3,)), [0, 0, 0])
+    with pytest.raises(pb.ValidationError):
+        pb.fuzzy_dice(z, z)
+    with pytest.raises(pb.ValidationError):
+        pb.prob_iou(z, z)
+    s = pb.ProbMask(pb.GridSpec((3,)), [0.2, 0.8, 0.5])
+    assert pb.fuzzy_dice(s, s) == 1.0 and pb.prob_iou(s, s) == 1.0
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        g = pb.GridSpec((10,))
+        x, y = pb.ProbMask(g, rng.uniform(size=10)), pb.ProbMask(g, rng.uniform(size=10))
+        d, j = pb.fuzzy_dice(x, y), pb.prob_iou(x, y)
+        assert d == pytest.approx(pb.fuzzy_dice(y, x), abs=1e-13)
+        assert d == pytest.approx(2 * j / (1 + j), abs=1e-12)
 
 
 def test_chain_pair_single_identical_empty(pb):
