@@ -78,7 +78,10 @@ const char* pidb_last_error(void);
  *   mass[i]      = sum_x w(x) u_i(x)                     (depth.py:275)
  *   col_mean[0]  = sum_x w(x) S(x)     (= N * mean_mass_total, depth.py:264)
  * Outputs are additive over disjoint cell shards (multi-GPU: allreduce-sum).
- * Deterministic: fixed reduction order for a fixed device. */
+ * Deterministic: fixed reduction order for a fixed device.  Any n: up to
+ * 4096 members one HBM read (TMA tiles); wider ensembles take a two-read
+ * path (column sweep, then row sweep).  The workspace size depends on
+ * (n, m, dtype) and is shared by every streaming entry point below. */
 size_t pidb_pid_mean_workspace_bytes(int64_t n, int64_t m, int dtype);
 int pidb_pid_mean_partials(const void* u, int dtype, int64_t n, int64_t m,
                            int64_t ld, const double* w, double* row_plain,

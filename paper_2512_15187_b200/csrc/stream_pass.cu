@@ -31,9 +31,17 @@
 //   chunked_kernel (256 < n <= 4096): the tile is streamed in 256-row chunks
 //                  twice; touch 1 (columns) comes from HBM with an L2
 //                  evict_last hint, touch 2 (rows) re-reads the chunks from L2.
+// Wider ensembles (n > 4096) take the two-read path in stream_wide.cu.
 #include "common.cuh"
 
 namespace pidb {
+
+// stream_wide.cu: two-read fallback for n > 4096 members
+size_t wide_workspace(int64_t n, int64_t m, int dtype);
+int run_wide_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                  const double* w, const double* inv, double* out_row, double* out_mass,
+                  double* out_col, int64_t* out_nb, void* ws, size_t ws_bytes, void* stream);
+
 namespace {
 
 constexpr int kThreads = 512;
@@ -660,11 +668,9 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
                "row stride %lld must be >= m and a multiple of 16 bytes", (long long)ld);
   PIDB_REQUIRE((reinterpret_cast<uintptr_t>(u) & 15) == 0, "member matrix must be 16-byte aligned");
   Plan pl;
-  if (!make_plan(n, m, es, pl)) {
-    set_error("ensembles of %lld members are not supported by the streaming tile (max %d)",
-              (long long)n, kChunkMax * kChunkRows);
-    return PIDB_EUNSUPPORTED;
-  }
+  if (!make_plan(n, m, es, pl))
+    return run_wide_pass(mode, u, dtype, n, m, ld, w, inv, out_row, out_mass, out_col, out_nb, ws,
+                         ws_bytes, stream);
   const size_t need = workspace_bytes(pl, n);
   if (ws == nullptr || ws_bytes < need) {
     set_error("workspace too small: need %zu bytes, got %zu", need, ws_bytes);
@@ -699,7 +705,8 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
 
 size_t stream_pass_workspace(int64_t n, int64_t m, int dtype) {
   Plan pl;
-  if (!make_plan(n, m, dtype == PIDB_F32 ? 4 : 8, pl)) return 0;
+  if (n < 1 || m < 1) return 0;
+  if (!make_plan(n, m, dtype == PIDB_F32 ? 4 : 8, pl)) return wide_workspace(n, m, dtype);
   return workspace_bytes(pl, n);
 }
 

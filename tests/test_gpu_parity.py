@@ -357,6 +357,38 @@ def test_layouts_vs_oracle(pb, n, dims, weighted):
     np.testing.assert_array_equal(r.rank, ref["rank"])
 
 
+@pytest.mark.parametrize("n,dims,weighted,f64", [
+    (4097, (33, 31), True, False), (5000, (2100,), False, False), (4500, (65,), True, True),
+])
+def test_wide_ensembles_vs_oracle(pb, n, dims, weighted, f64):
+    """n > 4096 takes the two-read streaming path (stream_wide.cu)."""
+    U, w = make_fuzzy(3000 + n, n, dims, weighted)
+    if f64:
+        U = U.astype(np.float64) * 0.75
+    e = ens(pb, U, w, dims=dims)
+    ref = port.depth_pid_mean(U, w, workers=8)
+    r = pb.depth_pid_mean(e)
+    close(r.depth, ref["depth"], 1e-12)
+    np.testing.assert_array_equal(r.rank, ref["rank"])
+    close(pb.member_masses(e), ref["mass"], 1e-9)
+    ref = port.depth_pid(U, w, workers=8)
+    r = pb.depth_pid(e, algorithm="factorized")
+    close(r.depth, ref["depth"], 1e-12)
+    np.testing.assert_array_equal(r.rank, ref["rank"])
+    ref = port.depth_similarity(U, "dice", w, workers=8)
+    close(pb.depth_similarity_baseline(e, "dice").depth, ref["depth"], 1e-12)
+
+
+def test_wide_binary_eid(pb):
+    U, _ = make_binary(77, 4200, (20, 20), False)
+    e = ens(pb, U, dims=(20, 20))
+    in_in, in_out, depth, _ = exact.eid_fast(U)
+    r = pb.depth_eid(e)
+    assert np.array_equal(r.in_in, in_in) and np.array_equal(r.in_out, in_out)
+    assert np.array_equal(r.depth, depth)
+    np.testing.assert_array_equal(r.rank, exact.ranks(depth))
+
+
 def test_float64_members(pb):
     rng = np.random.default_rng(5)
     U = rng.uniform(size=(9, 123))  # float64 stays float64 (grid.py:103-104)
