@@ -58,4 +58,5 @@ def test_workspace_query_needs_no_gpu():
 
     lib = N.load()
     assert lib.pidb_pid_mean_workspace_bytes(200, 1 << 20, N.PIDB_F32) > 0
-    assert lib.pidb_pid_mean_workspace_bytes(100000, 10, N.PIDB_F32) == 0  # unsupported N
+    assert lib.pidb_pid_mean_workspace_bytes(100000, 10, N.PIDB_F32) > 0  # wide (two-read) path
+    assert lib.pidb_pid_mean_workspace_bytes(0, 10, N.PIDB_F32) == 0  # empty ensemble
