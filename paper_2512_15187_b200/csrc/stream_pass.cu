@@ -32,6 +32,8 @@
 //                  twice; touch 1 (columns) comes from HBM with an L2
 //                  evict_last hint, touch 2 (rows) re-reads the chunks from L2.
 // Wider ensembles (n > 4096) take the two-read path in stream_wide.cu.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace pidb {
@@ -57,6 +59,8 @@ constexpr int MODE_SIM = 3;   // similarity baselines: sum w*min(u, mean), masse
 struct StreamParams {
   int64_t n, m, tiles;
   int stages;
+  int cs, rpc;           // cluster size and member rows per CTA (cluster rows kernel)
+  int groups;            // row-partial groups reduced by finish_partials
   uint32_t stage_bytes;  // bytes of one tile (rows kernel) or chunk (chunked)
   int mode;
   const double* w;       // nullable
@@ -175,7 +179,7 @@ __device__ __forceinline__ void finish_partials(const StreamParams& p, int pncb,
   for (int r = warp; r < n; r += kWarps) {
     double a = 0.0, b = 0.0;
     int64_t nb = 0;
-    for (int g = lane; g < G; g += 32) {
+    for (int g = lane; g < p.groups; g += 32) {
       for (int cb = 0; cb < pncb; ++cb) {
         const double* src = p.part + ((size_t)g * pncb * n + cb * n + r) * 2;
         a += __ldcg(src);
@@ -236,8 +240,16 @@ __device__ __forceinline__ void finalize_tile(const StreamParams& p, const doubl
 }
 
 // ---------------------------------------------------------------------------
-// rows_kernel: n <= 256, ROWS = ceil(n / 16) rows per warp.
-template <typename T, int ROWS>
+// rows_kernel: ROWS = ceil(rows / 16) member rows per warp.
+//   CL = false: n <= 256, one CTA holds every member row of its tiles.
+//   CL = true : 256 < n <= 16 * 256.  A cluster of cs CTAs shares each tile,
+//     CTA rank r holds rows [r * rpc, (r + 1) * rpc).  Pass 1 yields the
+//     CTA's column partials, which are pushed to every CTA of the cluster
+//     with st.async (DSMEM, completing on the receiver's mbarrier); pass 2
+//     of the previous tile sums the cs partials in rank order (identical in
+//     every CTA) and sweeps the CTA's own rows.  One HBM read, no L2
+//     re-read, the row sums stay in registers as for n <= 256.
+template <typename T, int ROWS, bool CL>
 __global__ void __launch_bounds__(kThreads, 1)
     rows_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
   constexpr int EPC = Vec<T>::EPC;
@@ -254,29 +266,64 @@ __global__ void __launch_bounds__(kThreads, 1)
   double* red = sW + 2 * V;                             // [2][kWarps][V]
   unsigned* s_ticket = reinterpret_cast<unsigned*>(red + 2 * kWarps * V);
   double* s_col = reinterpret_cast<double*>(s_ticket + 2);
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(tail + 64);        // [4] (CL)
+  const uint32_t xoff =
+      ((smem_u32(s_col + kWarps) + 15u) & ~15u) - smem_u32(smem_raw);  // 16-B aligned
+  double* xbuf = reinterpret_cast<double*>(smem_raw + xoff);        // [4][cs][V] (CL)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = (int)p.n;
-  const int G = gridDim.x;
   const int mode = p.mode;
   const int sweep = mode == MODE_SIM ? MODE_MEAN : mode;  // pass-1 column kind
   const bool weighted = p.w != nullptr;
-  const int64_t my_tiles = p.tiles > blockIdx.x ? (p.tiles - 1 - blockIdx.x) / G + 1 : 0;
+  const int cs = CL ? p.cs : 1;
+  const uint32_t rank = CL ? cluster_rank() : 0u;
+  const int cid = (int)blockIdx.x / cs, ncl = (int)gridDim.x / cs;
+  const int r0 = (int)rank * (CL ? p.rpc : 0);
+  const int box = CL ? p.rpc : n;                          // rows per TMA box
+  const int nloc = CL ? max(0, min(n - r0, p.rpc)) : n;    // member rows of this CTA
+  const bool exch = CL && mode != MODE_MASS;
+  const int64_t my_tiles = p.tiles > cid ? (p.tiles - 1 - cid) / ncl + 1 : 0;
   const uint64_t pol = policy_evict_first();
+  const uint32_t xbytes = (uint32_t)cs * V * 8u;  // all cs partials of a tile
+  double col_acc = 0.0;
 
   if (tid == 0) {
     prefetch_tma_desc(&tmap);
     for (int s = 0; s < p.stages; ++s) mbar_init(&full[s], 1);
+    if (exch)
+      for (int s = 0; s < 4; ++s) mbar_init(&xbar[s], 1);
     fence_mbar_init();
+    if (exch)
+      for (int s = 0; s < 4 && s < my_tiles; ++s) mbar_arrive_expect_tx(&xbar[s], xbytes);
   }
   __syncthreads();
+  if constexpr (CL) cluster_sync();  // peers' mbarriers exist before any st.async
 
   auto issue = [&](int64_t j) {  // local tile j -> stage j % stages (thread 0)
     const int s = (int)(j % p.stages);
-    mbar_arrive_expect_tx(&full[s], (uint32_t)n * kRowBytes);
-    tma_load_2d(tiles + (size_t)s * p.stage_bytes, &tmap, (int32_t)((blockIdx.x + j * G) * V), 0,
+    mbar_arrive_expect_tx(&full[s], (uint32_t)box * kRowBytes);
+    tma_load_2d(tiles + (size_t)s * p.stage_bytes, &tmap, (int32_t)((cid + j * ncl) * V), r0,
                 &full[s], pol);
   };
+  // CL: push this CTA's column partials of tile j to every CTA of the
+  // cluster (16-byte st.async, completing on the receiver's mbarrier; this
+  // measured faster than one bulk copy per peer)
+  auto send = [&](const double* rd, int64_t j) {
+    const int slot = (int)(j & 3);
+    for (int v = tid; v < V / 2; v += kThreads) {
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int k = 0; k < kWarps; ++k) {
+        a += rd[k * V + 2 * v];
+        b += rd[k * V + 2 * v + 1];
+      }
+      const uint32_t la = smem_u32(xbuf + ((size_t)slot * cs + rank) * V + 2 * v);
+      const uint32_t lb = smem_u32(&xbar[slot]);
+      for (int c = 0; c < cs; ++c) st_async_f64x2(mapa(la, c), a, b, mapa(lb, c));
+    }
+  };
+
   if (tid == 0)
     for (int64_t j = 0; j < my_tiles && j < p.stages; ++j) issue(j);
 
@@ -284,24 +331,41 @@ __global__ void __launch_bounds__(kThreads, 1)
   int acc_nb[ROWS];
 #pragma unroll
   for (int k = 0; k < ROWS; ++k) { acc_row[k] = 0.0; acc_mass[k] = 0.0; acc_nb[k] = 0; }
-  double col_acc = 0.0;
 
   const int q = tid & (kChunks16 - 1), ph = tid / kChunks16;
   const uint32_t p1_off = (uint32_t)(ph * kRowBytes + q * 16);
   const uint32_t p2_off = (uint32_t)(warp * kRowBytes + lane * 8);
   const int cell = lane * EPL;
 
-  auto pass2 = [&](const unsigned char* st, int buf) {
+  auto pass2 = [&](const unsigned char* st, int buf, int64_t jt) {
     double s_l[EPL], w_l[EPL];
+    if (exch) {
+      // CL: every lane forms S for its own cells from the cs partials of
+      // tile jt (rank order, identical in every CTA of the cluster)
+      const int slot = (int)(jt & 3);
+      mbar_wait(&xbar[slot], (uint32_t)((jt >> 2) & 1));
+      const int64_t x0 = (cid + jt * ncl) * (int64_t)V;
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) {
-      s_l[e] = sS[buf * V + cell + e];
-      w_l[e] = sW[buf * V + cell + e];
+      for (int e = 0; e < EPL; ++e) {
+        const int64_t x = x0 + cell + e;
+        const double wx = x < p.m ? (p.w ? __ldg(p.w + x) : 1.0) : 0.0;
+        double S = 0.0;
+        for (int c = 0; c < cs; ++c) S += xbuf[((size_t)slot * cs + c) * V + cell + e];
+        s_l[e] = p.mode == MODE_SIM ? __ddiv_rn(S, (double)p.n) : wx * S;
+        w_l[e] = wx;
+        if (rank == 0 && warp == 0) col_acc = fma(wx, S, col_acc);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        s_l[e] = sS[buf * V + cell + e];
+        w_l[e] = sW[buf * V + cell + e];
+      }
     }
     const unsigned char* base = st + p2_off;
 #define PIDB_ROWS_LOOP(BODY)                                                \
   _Pragma("unroll") for (int k = 0; k < ROWS; ++k) {                        \
-    if (k < ROWS - 1 || warp + k * kWarps < n) {                            \
+    if (k < ROWS - 1 || warp + k * kWarps < nloc) {                         \
       const unsigned char* a = base + k * (kWarps * kRowBytes);             \
       double v[EPL];                                                        \
       if constexpr (sizeof(T) == 4) {                                       \
@@ -329,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #undef PIDB_ROWS_LOOP
   };
 
-  ColSweep<T> cs;
+  ColSweep<T> csw;
   int s_cur = 0, s_prev = 0;
   uint32_t par = 0;
   for (int64_t j = 0; j <= my_tiles; ++j) {
@@ -338,22 +402,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (have) {
       mbar_wait(&full[s_cur], par);
       if (mode != MODE_MASS) {
-        cs.reset();
-        cs.run(tiles + (size_t)s_cur * p.stage_bytes + p1_off, ph, n, sweep, p.inv, ph, n);
-        cs.combine(sweep);
+        csw.reset();
+        csw.run(tiles + (size_t)s_cur * p.stage_bytes + p1_off, ph, box, sweep, p.inv, r0 + ph,
+                n);
+        csw.combine(sweep);
         if (lane < 16) {
 #pragma unroll
-          for (int e = 0; e < EPC; ++e) rd[warp * V + q * EPC + e] = cs.part[e];
+          for (int e = 0; e < EPC; ++e) rd[warp * V + q * EPC + e] = csw.part[e];
         }
       }
     }
     __syncthreads();
     // tile j-2's stage was last read by pass 2 in the previous iteration
     if (tid == 0 && j >= 2 && j - 2 + p.stages < my_tiles) issue(j - 2 + p.stages);
-    if (have)
-      finalize_tile<V, 0>(p, rd, (blockIdx.x + j * G) * (int64_t)V, sS + (j & 1) * V,
+    if (exch) {
+      // every thread passed its wait for tile j-2 (previous iteration): re-arm
+      // that slot for tile j+2
+      if (tid == 0 && j >= 2 && j + 2 < my_tiles)
+        mbar_arrive_expect_tx(&xbar[(j - 2) & 3], xbytes);
+      if (have) send(rd, j);
+    } else if (have) {
+      finalize_tile<V, 0>(p, rd, (cid + j * ncl) * (int64_t)V, sS + (j & 1) * V,
                        sW + (j & 1) * V, mode != MODE_MASS, col_acc);
-    if (j >= 1) pass2(tiles + (size_t)s_prev * p.stage_bytes, (int)((j - 1) & 1));
+    }
+    if (j >= 1) pass2(tiles + (size_t)s_prev * p.stage_bytes, (int)((j - 1) & 1), j - 1);
     s_prev = s_cur;
     if (++s_cur == p.stages) { s_cur = 0; par ^= 1u; }
   }
@@ -361,19 +433,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   // rows -> global partials (part layout [grid][n][2])
 #pragma unroll
   for (int k = 0; k < ROWS; ++k) {
-    const int r = warp + k * kWarps;
+    const int rl = warp + k * kWarps;
     const double a = warp_sum(acc_row[k]);
     const double b = warp_sum(acc_mass[k]);
     int nb = acc_nb[k];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
-    if (lane == 0 && r < n) {
-      double* dst = p.part + ((size_t)blockIdx.x * n + r) * 2;
+    if (lane == 0 && rl < nloc) {
+      const int r = r0 + rl;
+      double* dst = p.part + ((size_t)cid * n + r) * 2;
       dst[0] = a;
       dst[1] = b;
-      if (p.mode == MODE_MASS && p.part_nb != nullptr) p.part_nb[(size_t)blockIdx.x * n + r] = nb;
+      if (p.mode == MODE_MASS && p.part_nb != nullptr) p.part_nb[(size_t)cid * n + r] = nb;
     }
   }
+  if constexpr (CL) cluster_sync();  // no CTA leaves while peers may still target its SMEM
   finish_partials(p, 1, col_acc, s_ticket, s_col);
 }
 
@@ -412,10 +486,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int mode = p.mode;
   const int sweep = mode == MODE_SIM ? MODE_MEAN : mode;  // pass-1 column kind
   const bool two_touch = mode != MODE_MASS;
-  const int loads_per_tile = two_touch ? 2 * C : C;
   const bool weighted = p.w != nullptr;
   const int64_t my_tiles = p.tiles > blockIdx.x ? (p.tiles - 1 - blockIdx.x) / G + 1 : 0;
-  const int64_t total_loads = my_tiles * loads_per_tile;
   const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
 
   if (tid == 0) {
@@ -425,18 +497,56 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
 
-  auto issue = [&](int64_t qq) {  // qq-th chunk load of this CTA (thread 0)
-    const int b = (int)(qq % kChunkBufs);
-    const int64_t j = qq / loads_per_tile;
-    const int i = (int)(qq - j * loads_per_tile);
-    const bool second = i >= C;
-    const int c = second ? i - C : i;
-    mbar_arrive_expect_tx(&full[b], kChunkBytes);
-    tma_load_2d(bufs + (size_t)b * kChunkBytes, &tmap, (int32_t)((blockIdx.x + j * G) * V),
-                c * kChunkRows, &full[b], (two_touch && !second) ? pol_keep : pol_drop);
+  // Chunk schedule.  Uses per tile: touch 1 visits chunks 0..C-1, touch 2
+  // visits C-1..0, so the last R = min(C, kChunkBufs) chunks of touch 1 are
+  // still resident when touch 2 starts and are reused without a reload
+  // (n <= 768: one touch of HBM and no L2 re-read at all).  Every thread runs
+  // the same deterministic schedule; thread 0 issues the TMA loads.  A
+  // buffer is refilled (next load in use order) as soon as its chunk has no
+  // later use, so two uses of lookahead stay in flight across touches/tiles.
+  const int R = two_touch ? min(C, kChunkBufs) : 0;
+  const int P = two_touch ? 2 * C : C;  // uses per tile
+  // small FIFOs of 2-bit buffer ids packed in registers
+  uint32_t fq = 0, fq_n = kChunkBufs;  // free buffers
+#pragma unroll
+  for (int b = 0; b < kChunkBufs; ++b) fq |= (uint32_t)b << (2 * b);
+  uint32_t lq = 0, lq_n = 0;  // buffers of issued, not yet consumed loads
+  uint32_t rbuf = 0;  // buffers of the resident chunks C-R .. C-1, per tile (mod 4:
+                      // at most 3 tiles hold buffers at a time)
+  uint32_t ph_bits = 0;       // per-buffer mbarrier parity
+  int64_t lj = 0;        // next load: tile lj, use position lpos
+  int lpos = 0;
+  auto needs_load = [&](int pos) { return pos < C || (P - 1 - pos) < C - R; };
+  // (single touch: P == C, every use loads)
+  auto issue_loads = [&]() {
+    while (fq_n > 0 && lj < my_tiles) {
+      if (!needs_load(lpos)) {
+        if (++lpos == P) { lpos = 0; ++lj; }
+        continue;
+      }
+      const uint32_t b = fq & 3u;
+      fq >>= 2;
+      --fq_n;
+      lq |= b << (2 * lq_n);
+      ++lq_n;
+      // touch 1 walks up; the row sweep (touch 2, or the only touch) walks down
+      const bool first_touch = two_touch && lpos < C;
+      const int c = first_touch ? lpos : P - 1 - lpos;
+      if (first_touch && c >= C - R) {
+        const int sh = 2 * ((int)(lj & 3) * kChunkBufs + c - (C - R));
+        rbuf = (rbuf & ~(3u << sh)) | (b << sh);
+      }
+      if (tid == 0) {
+        // keep (evict_last) only chunks that touch 2 re-reads from L2
+        const bool keep = two_touch && first_touch && c < C - R;
+        mbar_arrive_expect_tx(&full[b], kChunkBytes);
+        tma_load_2d(bufs + (size_t)b * kChunkBytes, &tmap, (int32_t)((blockIdx.x + lj * G) * V),
+                    c * kChunkRows, &full[b], keep ? pol_keep : pol_drop);
+      }
+      if (++lpos == P) { lpos = 0; ++lj; }
+    }
   };
-  if (tid == 0)
-    for (int64_t qq = 0; qq < total_loads && qq < kChunkBufs; ++qq) issue(qq);
+  issue_loads();
 
   double acc_row[CMAX], acc_mass[CMAX];
   int acc_nb[CMAX];
@@ -450,16 +560,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t b_off = (uint32_t)(b_rr * kRowBytes + b_half * (kRowBytes / 2));
   const int b_rot = b_rr & 7;
 
-  int64_t qq = 0;  // chunk loads consumed
-  auto next_chunk = [&]() -> const unsigned char* {
-    const int b = (int)(qq % kChunkBufs);
-    mbar_wait(&full[b], (uint32_t)((qq / kChunkBufs) & 1));
-    return bufs + (size_t)b * kChunkBytes;
+  uint32_t cur_b = 0;
+  auto use_chunk = [&](int64_t j, int pos) -> const unsigned char* {
+    if (needs_load(pos)) {
+      cur_b = lq & 3u;
+      lq >>= 2;
+      --lq_n;
+      mbar_wait(&full[cur_b], (ph_bits >> cur_b) & 1u);
+      ph_bits ^= 1u << cur_b;
+    } else {
+      cur_b = (rbuf >> (2 * ((int)(j & 3) * kChunkBufs + (P - 1 - pos) - (C - R)))) & 3u;
+    }
+    return bufs + (size_t)cur_b * kChunkBytes;
   };
-  auto release_chunk = [&]() {
+  auto release_chunk = [&](int pos) {
     __syncthreads();  // everyone is done with this buffer
-    if (tid == 0 && qq + kChunkBufs < total_loads) issue(qq + kChunkBufs);
-    ++qq;
+    const bool reused = two_touch && pos < C && pos >= C - R;
+    if (!reused) {
+      fq |= cur_b << (2 * fq_n);
+      ++fq_n;
+      issue_loads();
+    }
   };
 
   ColSweep<T> cs;
@@ -468,9 +589,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (two_touch) {  // ------------------------------ touch 1: column sweep
       cs.reset();
       for (int c = 0; c < C; ++c) {
-        const unsigned char* st = next_chunk();
+        const unsigned char* st = use_chunk(j, c);
         cs.run(st + a_off, ph, kChunkRows, sweep, p.inv, c * kChunkRows + ph, n);
-        release_chunk();
+        release_chunk(c);
       }
       cs.combine(sweep);
       if (lane < 16) {
@@ -485,9 +606,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const double* S = sS + b_half * HALF;
     const double* W = sW + b_half * HALF;
 #pragma unroll
-    for (int c = 0; c < CMAX; ++c) {
+    for (int c = CMAX - 1; c >= 0; --c) {  // the row sweep walks the chunks backwards
       if (c < C) {
-        const unsigned char* line = next_chunk() + b_off;
+        const int pos = P - 1 - c;
+        const unsigned char* line = use_chunk(j, pos) + b_off;
         if (c * kChunkRows + b_rr < n) {
           double ar[EPC], am[EPC];
           int nb = 0;
@@ -535,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           acc_mass[c] += tm;
           acc_nb[c] += nb;
         }
-        release_chunk();
+        release_chunk(pos);
       }
     }
   }
@@ -579,14 +701,32 @@ constexpr int kChunkMax = 16;  // n <= 4096
 
 struct Plan {
   bool chunked;
+  int cs, rpc;  // cs > 1: cluster rows kernel
   int rows, stages, grid, box_rows;
   uint32_t stage_bytes;
   size_t smem;
   int64_t tiles;
 };
 
-size_t rows_tail(int V) {
-  return 128 + (size_t)4 * V * 8 + (size_t)2 * kWarps * V * 8 + 16 + kWarps * 8 + 64;
+size_t rows_tail(int V, int cs) {
+  return 128 + (size_t)4 * V * 8 + (size_t)2 * kWarps * V * 8 + 16 + kWarps * 8 + 64 +
+         (cs > 1 ? (size_t)4 * cs * V * 8 + 16 : 0);
+}
+
+// Cluster size for 256 < n (0 = chunked kernel), from measurements on B200
+// (tools/prof_k5.py, 256^3 cells): pairs of CTAs win for
+// n <= 512 and 8-CTA clusters for 1536 < n <= 2048; in between the chunked
+// kernel is faster.  PIDB_CLUSTER overrides (tuning).
+int cluster_size_for(int64_t n) {
+  int cs = 0;
+  if (n <= 512) cs = 2;
+  else if (n > 1536 && n <= 2048) cs = 8;
+  if (const char* e = std::getenv("PIDB_CLUSTER")) {
+    const int v = std::atoi(e);
+    if (v >= (int)((n + 255) / 256) && v <= 16) cs = v;
+    if (v == 0) cs = 0;  // disable: chunked kernel
+  }
+  return cs;
 }
 size_t chunked_smem(int V) {
   return 1024 + (size_t)kChunkBufs * kChunkBytes + 64 + (size_t)(2 + kWarps) * V * 8 + 16 +
@@ -598,12 +738,35 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
   const int V = kRowBytes / esize;
   pl.tiles = (m + V - 1) / V;
   pl.grid = (int)std::min<int64_t>(pl.tiles, sm_count());
+  pl.cs = 1;
+  pl.rpc = (int)n;
+  if (n > 256 && n <= 16 * 256) {
+    const int cs = cluster_size_for(n);
+    if (cs >= 2 && cs <= 16) {
+      pl.chunked = false;
+      pl.cs = cs;
+      pl.grid = (int)std::max<int64_t>(
+          cs, std::min<int64_t>(pl.tiles * cs, sm_count()) / cs * cs);
+      pl.rpc = (int)((n + cs - 1) / cs);
+      pl.rows = (pl.rpc + kWarps - 1) / kWarps;
+      pl.box_rows = pl.rpc;
+      pl.stage_bytes = (uint32_t)align_up((size_t)pl.rpc * kRowBytes, 1024);
+      const size_t tb = rows_tail(V, cs) + 1024;
+      pl.stages = (int)std::min<size_t>(kMaxStages, (kSmemBudget - tb) / pl.stage_bytes);
+      if (pl.stages >= 3) {
+        pl.smem = (size_t)pl.stages * pl.stage_bytes + tb;
+        return true;
+      }
+      pl.cs = 1;
+      pl.rpc = (int)n;
+    }
+  }
   if (n <= 256) {
     pl.chunked = false;
     pl.rows = (int)((n + kWarps - 1) / kWarps);
     pl.box_rows = (int)n;
     pl.stage_bytes = (uint32_t)align_up((size_t)n * kRowBytes, 1024);
-    const size_t tb = rows_tail(V) + 1024;
+    const size_t tb = rows_tail(V, 1) + 1024;
     pl.stages = (int)std::min<size_t>(kMaxStages, (kSmemBudget - tb) / pl.stage_bytes);
     if (pl.stages < 3) return false;
     pl.smem = (size_t)pl.stages * pl.stage_bytes + tb;
@@ -635,8 +798,57 @@ int launch(K kern, const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cuda
   return PIDB_OK;
 }
 
+// cluster launch; grid = co-resident clusters (persistent) x cs
+template <typename K>
+int launch_cluster(K kern, const CUtensorMap& tm, StreamParams& sp, const Plan& pl,
+                   cudaStream_t st) {
+  PIDB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+  if (pl.cs > 8) PIDB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)pl.cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)(pl.grid / pl.cs * pl.cs));
+  int active = 0;
+  PIDB_CUDA(cudaOccupancyMaxActiveClusters(&active, kern, &cfg));
+  if (active < 1) {
+    set_error("no co-resident cluster of %d CTAs for the streaming kernel", pl.cs);
+    return PIDB_EUNSUPPORTED;
+  }
+  const int64_t ncl = std::min<int64_t>(std::min<int64_t>(active, pl.grid / pl.cs), sp.tiles);
+  cfg.gridDim = dim3((unsigned)(ncl * pl.cs));
+  if (std::getenv("PIDB_DEBUG"))
+    std::fprintf(stderr, "pidb: cluster %d x %lld CTAs (active %d), rpc %d, stages %d, smem %zu\n",
+                 pl.cs, (long long)ncl, active, pl.rpc, pl.stages, pl.smem);
+  sp.groups = (int)ncl;
+  PIDB_CUDA(cudaLaunchKernelEx(&cfg, kern, tm, sp));
+  PIDB_LAUNCH_CHECK("cluster stream kernel");
+  return PIDB_OK;
+}
+
 template <typename T>
 int launch_typed(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream_t st) {
+  if (pl.cs > 1) {
+    switch (pl.rows) {
+#define PIDB_CL_CASE(R) \
+  case R: return launch_cluster(rows_kernel<T, R, true>, tm, sp, pl, st);
+      PIDB_CL_CASE(1) PIDB_CL_CASE(2) PIDB_CL_CASE(3) PIDB_CL_CASE(4)
+      PIDB_CL_CASE(5) PIDB_CL_CASE(6) PIDB_CL_CASE(7) PIDB_CL_CASE(8)
+      PIDB_CL_CASE(9) PIDB_CL_CASE(10) PIDB_CL_CASE(11) PIDB_CL_CASE(12)
+      PIDB_CL_CASE(13) PIDB_CL_CASE(14) PIDB_CL_CASE(15) PIDB_CL_CASE(16)
+#undef PIDB_CL_CASE
+    }
+    set_error("unsupported rows per warp %d", pl.rows);
+    return PIDB_EUNSUPPORTED;
+  }
+  sp.groups = pl.grid;
   if (pl.chunked) {
     const int C = (int)((sp.n + kChunkRows - 1) / kChunkRows);
     if (C <= 4) return launch(chunked_kernel<T, 4>, tm, sp, pl, st);
@@ -645,7 +857,7 @@ int launch_typed(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaSt
   }
   switch (pl.rows) {
 #define PIDB_ROWS_CASE(R) \
-  case R: return launch(rows_kernel<T, R>, tm, sp, pl, st);
+  case R: return launch(rows_kernel<T, R, false>, tm, sp, pl, st);
     PIDB_ROWS_CASE(1) PIDB_ROWS_CASE(2) PIDB_ROWS_CASE(3) PIDB_ROWS_CASE(4)
     PIDB_ROWS_CASE(5) PIDB_ROWS_CASE(6) PIDB_ROWS_CASE(7) PIDB_ROWS_CASE(8)
     PIDB_ROWS_CASE(9) PIDB_ROWS_CASE(10) PIDB_ROWS_CASE(11) PIDB_ROWS_CASE(12)
@@ -689,6 +901,7 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
   base += 256;
   sp.n = n; sp.m = m; sp.tiles = pl.tiles;
   sp.stages = pl.stages; sp.stage_bytes = pl.stage_bytes; sp.mode = mode;
+  sp.cs = pl.cs; sp.rpc = pl.rpc; sp.groups = pl.grid;
   sp.w = w; sp.inv = inv;
   sp.part = reinterpret_cast<double*>(base);
   base += align_up((size_t)pl.grid * 2 * n * 2 * sizeof(double), 256);
