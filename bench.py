@@ -248,6 +248,20 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def ncu_traffic(workload, world):
+    """DRAM bytes (read + write) per K5 launch from the committed ncu capture of
+    the same workload (profiles/r01_traffic.json), or None."""
+    if world != 1:
+        return None
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                               "r01_traffic.json")) as fh:
+            t = json.load(fh).get(workload)
+        return None if t is None else t["dram_read_bytes"] + t["dram_write_bytes"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def metric_name(method):
     return "member-voxels/sec for PID-mean" if method == "pid-mean" else "member-voxels/sec for PID"
 
@@ -305,7 +319,8 @@ def run_ours(args, rank, world, local, pg):
                    if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "kernel": "stream_pass_kernel (K5, pidb_pid_mean_partials)",
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"] if achieved else None, "traffic": None,
+                     "frac": achieved / pk["hbm_gbs"] if achieved else None,
+                     "traffic": ncu_traffic(args.workload, world),
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "kernel_ms": kms, "launches_timed": klaunch, "peak_src": pk["src"]},
         "gpu_launches": launches_per_step * args.steps,
