@@ -229,6 +229,20 @@ int pidb_synth_ellipsoids(float* out, int64_t n, int64_t res, int64_t ld,
 int pidb_synth_disks(float* out, int64_t n, int64_t res, int64_t ld,
                      const double* params, double sigma2, void* stream);
 
+/* ---------------------------------------------------------------- K10 ---
+ * Contour-boxplot band envelopes, one pass over the kmax deepest members.
+ * Replaces the member loop of build_boxplot
+ * (/root/reference/pkg/src/fuzzdepth/boxplot.py:43-101).
+ *   member_by_rank: device int64[kmax], matrix row of the member of rank r
+ *   cutoffs       : device int64[nbands], ascending k_b = ceil(p_b * n) <= kmax
+ *   unions/inters : device uint8[nbands][m]; band b's OR / AND of the masks
+ *                   {u >= threshold} (threshold rounded to the member dtype,
+ *                   grid.py:264-268) over the members of rank < k_b. */
+int pidb_band_envelopes(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                        const int64_t* member_by_rank, int64_t kmax, double threshold,
+                        const int64_t* cutoffs, int nbands, uint8_t* unions,
+                        uint8_t* inters, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

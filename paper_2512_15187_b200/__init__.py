@@ -46,10 +46,42 @@ from .grid import (
 )
 from .inclusion import fuzzy_dice, prob_inclusion, prob_iou, subset_epsilon
 from .reduction import gram_block
+from .fuzzify import ScalarField, default_width, fuzzy_isocontour, hard_isocontour, normalize_density
+from .boxplot import Band, BoxplotArtifact, build_boxplot, emit_slice_images, write_pgm
+from .consistency import RankScatter, kendall_tau, pearson, rank_scatter, stability_test
+from .io import (manifest_guarantees_binary, read_depth_csv, read_manifest, read_volume,
+                 stage_manifest, volume_header, write_boxplot_artifact, write_depth_csv,
+                 write_manifest, write_scatter_csv, write_volume)
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "Band",
+    "BoxplotArtifact",
+    "RankScatter",
+    "ScalarField",
+    "build_boxplot",
+    "default_width",
+    "emit_slice_images",
+    "fuzzy_isocontour",
+    "hard_isocontour",
+    "kendall_tau",
+    "manifest_guarantees_binary",
+    "normalize_density",
+    "pearson",
+    "rank_scatter",
+    "read_depth_csv",
+    "read_manifest",
+    "read_volume",
+    "stability_test",
+    "stage_manifest",
+    "volume_header",
+    "write_boxplot_artifact",
+    "write_depth_csv",
+    "write_manifest",
+    "write_pgm",
+    "write_scatter_csv",
+    "write_volume",
     "BinaryMask",
     "CV_WARN_THRESHOLD",
     "DegenerateEnsembleError",

@@ -71,6 +71,8 @@ SIGNATURES: dict[str, tuple] = {
     "pidb_validate": (_int, [_p, _int, _i64, _i64, _i64, _int, _p, _p]),
     "pidb_synth_ellipsoids": (_int, [_p, _i64, _i64, _i64, _p, _dbl, _p]),
     "pidb_synth_disks": (_int, [_p, _i64, _i64, _i64, _p, _dbl, _p]),
+    "pidb_band_envelopes": (_int, [_p, _int, _i64, _i64, _i64, _p, _i64, _dbl, _p, _int, _p, _p,
+                                   _p]),
 }
 
 # Entry points declared in pidb.h whose kernels are still being brought up.

@@ -394,7 +394,7 @@ def depth_similarity_baseline(ensemble, measure: str, workers: int | None = None
 
 def compare_pid_vs_mean(ensemble, workers: int | None = None) -> dict:
     """Exact PID vs PID-mean: depth error and rank agreement (depth.py:328-346)."""
-    from scipy import stats
+    from .consistency import kendall_tau, pearson
 
     de = stage(ensemble)
     if de.n < 2:
@@ -402,20 +402,11 @@ def compare_pid_vs_mean(ensemble, workers: int | None = None) -> dict:
     exact = depth_pid(de, workers)
     approx = depth_pid_mean(de, workers)
     err = np.abs(exact.depth - approx.depth)
-
-    def _pearson(x, y):
-        dx = np.asarray(x, dtype=np.float64) - np.mean(x)
-        dy = np.asarray(y, dtype=np.float64) - np.mean(y)
-        sx, sy = float(np.sum(dx * dx)), float(np.sum(dy * dy))
-        if sx == 0.0 or sy == 0.0:
-            raise ValidationError("pearson undefined: an input has zero variance")
-        return float(np.sum(dx * dy) / np.sqrt(sx * sy))
-
     return {
         "max_abs_error": float(err.max()),
         "mean_abs_error": float(err.mean()),
-        "rank_pearson": _pearson(exact.rank, approx.rank),
-        "rank_kendall": float(stats.kendalltau(exact.rank, approx.rank, variant="b").statistic),
+        "rank_pearson": pearson(exact.rank, approx.rank),
+        "rank_kendall": kendall_tau(exact.rank, approx.rank),
         "cv_mass": approx.cv_mass,
     }
 

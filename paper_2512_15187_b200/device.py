@@ -159,6 +159,17 @@ class DeviceEnsemble:
         return cls.from_tensor(torch.from_numpy(arr), grid.weights, ids,
                                tuple(grid.dims), validate=False, device=device)
 
+    def subset(self, indices: Sequence[int]) -> "DeviceEnsemble":
+        """Members ``indices`` in the given order (grid.py Ensemble.subset);
+        one device-side row gather, same grid and weights."""
+        idx = torch.as_tensor(list(indices), dtype=torch.int64, device=self.device)
+        if idx.numel() == 0:
+            raise DegenerateEnsembleError("ensemble needs at least one member")
+        return DeviceEnsemble(self.values.index_select(0, idx).contiguous(), self.m, self.dims,
+                              tuple(self.ids[int(i)] for i in indices), self.weights,
+                              self.weights_host, process_group=self.process_group,
+                              cell_range=self.cell_range)
+
     # ------------------------------------------------------------- helpers
     def workspace(self, nbytes: int) -> torch.Tensor:
         """Zero-initialised per-device workspace (the kernels leave their

@@ -166,5 +166,60 @@ def main():
          dice=np.array(dice), iou=np.array(iou))
 
 
+def tools_golden():
+    """Host-side formats and callers of the depth path: CSV bytes, fuzzify,
+    boxplot envelopes / slice images, stability and rank scatter."""
+    import json
+    import tempfile
+
+    from fuzzdepth import boxplot as bx
+    from fuzzdepth import consistency as cons
+    from fuzzdepth import fuzzify as fz
+    from fuzzdepth import io as fio
+
+    z = np.load(OUT / "fuzzy_07.npz")
+    U, w, dims = z["U"], z["w"], tuple(int(d) for d in z["dims"])
+    e = ensemble(U, w, dims)
+    pid = fd.depth_pid(e)
+    pm = fd.depth_pid_mean(e)
+    with tempfile.TemporaryDirectory() as td:
+        fio.write_depth_csv(pid, f"{td}/d.csv", workers=1)
+        csv_bytes = open(f"{td}/d.csv", "rb").read()
+        art = bx.build_boxplot(e, pid, [0.25, 0.5, 1.0], 0.5, 2)
+        pgms = [open(p, "rb").read() for p in bx.emit_slice_images(art, e, 2, 3, td)]
+        pgms += [open(p, "rb").read() for p in bx.emit_slice_images(art, e, 0, 8, td)]
+    (OUT / "tools_depth_pid.csv").write_bytes(csv_bytes)
+    arrays = {"pgm_%d" % i: np.frombuffer(b, dtype=np.uint8) for i, b in enumerate(pgms)}
+    for b, band in enumerate(art.bands):
+        arrays[f"union_{b}"] = band.union.bits
+        arrays[f"inter_{b}"] = band.intersection.bits
+    rng = np.random.default_rng(11)
+    field = rng.normal(size=(9, 10, 11))
+    g = fd.GridSpec(field.shape)
+    f = fz.ScalarField(g, field)
+    arrays["field"] = field
+    arrays["fz_iso"] = fz.fuzzy_isocontour(f, 0.3, 0.7).values
+    arrays["fz_iso_default"] = fz.fuzzy_isocontour(f, -0.2, fz.default_width(f)).values
+    arrays["fz_sub"] = fz.hard_isocontour(f, 0.1).bits
+    arrays["fz_minmax"] = fz.normalize_density(f, "minmax").values
+    arrays["fz_sbm"] = fz.normalize_density(fz.ScalarField(g, np.abs(field)), "scale-by-max").values
+    planes = (rng.uniform(size=(4, 12, 13)) < 0.6)
+    arrays["planes"] = planes
+    arrays["edges"] = np.stack([bx._contour_cells(p) for p in planes])
+    np.savez_compressed(OUT / "tools.npz", **arrays)
+    meta = {
+        "bands": [{"percentile": b.percentile, "member_ids": list(b.member_ids)} for b in art.bands],
+        "median_id": art.median_id, "outlier_ids": list(art.outlier_ids),
+        "stability_pid_3": cons.stability_test(e, "pid", 3),
+        "stability_pidmean_0": cons.stability_test(e, "pid-mean", 0),
+        "scatter": [list(r) for r in cons.rank_scatter(pid, pm).rows],
+        "scatter_stats": [cons.rank_scatter(pid, pm).pearson, cons.rank_scatter(pid, pm).kendall],
+        "ids": list(e.ids),
+    }
+    (OUT / "tools.json").write_text(json.dumps(meta, indent=1) + "\n")
+    print("tools", sorted(arrays))
+
+
 if __name__ == "__main__":
     main()
+    tools_golden()
