@@ -204,9 +204,26 @@ def cpu_reference(U, method, workers):
     t0 = time.perf_counter()
     if method == "pid-mean":
         port.depth_pid_mean(U, None, workers=workers)
+    elif method == "eid":
+        port.depth_eid(U, None, workers=workers)
     else:
         port.depth_pid(U, None, workers=workers)
     return time.perf_counter() - t0
+
+
+def cpu_pair_baseline(U, method, n_full, m_full, what):
+    """oracle.port on a bounded sample of an O(N^2 M) workload: measured
+    pair-voxels/s plus the full-size time extrapolated from it (labelled)."""
+    workers = os.cpu_count() or 1
+    sec = cpu_reference(U, method, workers)
+    pv = U.shape[0] ** 2 * U.shape[1] / sec
+    return {"value": U.shape[0] * U.shape[1] / sec, "unit": "member-voxels/s",
+            "pair_voxels_per_s": pv, "cores": workers, "kind": "port",
+            "sample": f"{U.shape[0]} members x {U.shape[1]} cells of {what}; oracle.port {method} "
+                      f"(numpy/OpenBLAS fp64 Gram tiles), ThreadPool({workers})",
+            "seconds": sec,
+            "extrapolated_full_seconds": n_full ** 2 * m_full / pv,
+            "extrapolation": "full-size time = N^2 M / measured pair-voxels/s (not measured)"}
 
 
 # ------------------------------------------------------------ reference arm
@@ -463,6 +480,12 @@ def run_pid_secondary(args, rank, world, pg, dev, pk):
     out["ms_per_depth"] = out["factorized"]["ms_per_depth"]
     out["value"] = out["factorized"]["value"]
     out["algorithm"] = "factorized (exact, default)"
+    if rank == 0 and world == 1 and not args.no_cpu:
+        planes = 8
+        lo = (res // 2 - planes // 2) * res * res
+        U = de.values[: args.ref_pid_members, lo:lo + planes * res * res].cpu().numpy()
+        out["cpu_baseline"] = cpu_pair_baseline(U, "pid", n, res ** 3,
+                                                f"{planes} central planes of cfg4")
     del de
     torch.cuda.empty_cache()
     return out
@@ -489,6 +512,10 @@ def run_eid_secondary(args, dev, pk):
     D.KERNEL_EVENTS = None
     kg, _ = kernel_ms(ev, "pidb_gram_i8")
     km, _ = kernel_ms(ev, "pidb_member_masses")
+    cpu = None
+    if not args.no_cpu:
+        U = de.values[:100, : res * res].cpu().numpy()
+        cpu = cpu_pair_baseline(U, "eid", n, res * res, "cfg2 (full 512^2 grid)")
     m = res * res
     ops = 2.0 * n * n * m
     out = {"workload": "cfg2: eID, 500 binary contours 512^2 (bit-exact integer path)",
@@ -500,6 +527,8 @@ def run_eid_secondary(args, dev, pk):
                              "kernel_ms": kg, "algorithmic_ops": ops,
                              "peak_src": "cuBLAS INT8 probe (torch._int_mm 8192^3)"},
            "masses_ms": km}
+    if cpu is not None:
+        out["cpu_baseline"] = cpu
     del de
     torch.cuda.empty_cache()
     return out
