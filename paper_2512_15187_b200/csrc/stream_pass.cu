@@ -51,6 +51,10 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kRowBytes = 256;          // bytes of one member row per tile
 constexpr int kChunks16 = kRowBytes / 16;
 constexpr int kPhases = kThreads / kChunks16;  // row phases of the column sweep
+// block size of the rows kernels (640 threads was measured 11% slower on
+// cfg5: the 96-register budget costs more than the extra warps bring)
+constexpr int kRowsThreads = 512;
+constexpr int kRowsWarps = kRowsThreads / 32;
 constexpr int MODE_MEAN = 0;
 constexpr int MODE_COLS = 1;
 constexpr int MODE_MASS = 2;  // masses (+ non-binary count): row sweep only
@@ -102,8 +106,9 @@ __device__ __forceinline__ bool is_nonbinary(double x) { return !(x == 0.0 || x 
 // Column sweep over 256-byte rows: this thread's 16-byte chunk of rows
 // r0, r0 + kPhases, ... < r_end, starting at `pa`.  fp32 MODE_MEAN uses the
 // Fast2Sum state; otherwise part[] += iv(row) * u in fp64.
-template <typename T>
+template <typename T, int NT = kThreads>
 struct ColSweep {
+  static constexpr int kPh = NT / kChunks16;  // row phases
   static constexpr int EPC = Vec<T>::EPC;
   float2 sh01, sh23, sc01, sc23;
   double part[EPC];
@@ -119,7 +124,7 @@ struct ColSweep {
     if constexpr (sizeof(T) == 4) {
       if (mode == MODE_MEAN) {
 #pragma unroll 4
-        for (int r = r0; r < r_end; r += kPhases, pa += kPhases * kRowBytes) {
+        for (int r = r0; r < r_end; r += kPh, pa += kPh * kRowBytes) {
           const float4 v = Vec<float>::loadf(pa);
           fast2sum_acc2(sh01, sc01, make_float2(v.x, v.y));
           fast2sum_acc2(sh23, sc23, make_float2(v.z, v.w));
@@ -128,7 +133,7 @@ struct ColSweep {
       }
     }
 #pragma unroll 4
-    for (int r = r0; r < r_end; r += kPhases, rg += kPhases, pa += kPhases * kRowBytes) {
+    for (int r = r0; r < r_end; r += kPh, rg += kPh, pa += kPh * kRowBytes) {
       double v[EPC];
       Vec<T>::load(pa, v);
       const double iv = mode == MODE_MEAN ? 1.0 : (rg < n ? __ldg(inv + rg) : 0.0);
@@ -154,6 +159,7 @@ struct ColSweep {
 
 // CTA column partial -> global; the last CTA to finish reduces every CTA's
 // partials in a fixed order (grid, then half) and resets the counter.
+template <int NT>
 __device__ __forceinline__ void finish_partials(const StreamParams& p, int pncb, double col_acc,
                                                 unsigned* s_ticket, double* s_col) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -165,7 +171,7 @@ __device__ __forceinline__ void finish_partials(const StreamParams& p, int pncb,
     __syncthreads();
     if (tid == 0) {
       double t = 0.0;
-      for (int k = 0; k < kWarps; ++k) t += s_col[k];
+      for (int k = 0; k < (NT / 32); ++k) t += s_col[k];
       p.part_col[blockIdx.x] = t;
     }
   }
@@ -176,7 +182,7 @@ __device__ __forceinline__ void finish_partials(const StreamParams& p, int pncb,
   if (*s_ticket != (unsigned)(G - 1)) return;
 
   __threadfence();
-  for (int r = warp; r < n; r += kWarps) {
+  for (int r = warp; r < n; r += (NT / 32)) {
     double a = 0.0, b = 0.0;
     int64_t nb = 0;
     for (int g = lane; g < p.groups; g += 32) {
@@ -215,11 +221,11 @@ __device__ __forceinline__ void finish_partials(const StreamParams& p, int pncb,
 // EPC_PERM > 0 stores cell (8 chunks of EPC per half row) at the
 // element-major slot half*V/2 + e*8 + chunk, which makes the chunked
 // kernel's row-rotated reads bank-conflict free.
-template <int V, int EPC_PERM>
+template <int V, int EPC_PERM, int NT = kThreads>
 __device__ __forceinline__ void finalize_tile(const StreamParams& p, const double* rd, int64_t x0,
                                               double* sS, double* sW, bool colsum,
                                               double& col_acc) {
-  for (int v = threadIdx.x; v < V; v += kThreads) {
+  for (int v = threadIdx.x; v < V; v += NT) {
     const int64_t x = x0 + v;
     const double wx = x < p.m ? (p.w ? __ldg(p.w + x) : 1.0) : 0.0;
     int slot = v;
@@ -231,7 +237,7 @@ __device__ __forceinline__ void finalize_tile(const StreamParams& p, const doubl
     if (colsum) {
       double S = 0.0;
 #pragma unroll
-      for (int k = 0; k < kWarps; ++k) S += rd[k * V + v];
+      for (int k = 0; k < NT / 32; ++k) S += rd[k * V + v];
       // MODE_SIM keeps the mean mask value (mean_mask, grid.py:251-261)
       sS[slot] = p.mode == MODE_SIM ? __ddiv_rn(S, (double)p.n) : wx * S;
       col_acc = fma(wx, S, col_acc);
@@ -250,7 +256,7 @@ __device__ __forceinline__ void finalize_tile(const StreamParams& p, const doubl
 //     every CTA) and sweeps the CTA's own rows.  One HBM read, no L2
 //     re-read, the row sums stay in registers as for n <= 256.
 template <typename T, int ROWS, bool CL>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kRowsThreads, 1)
     rows_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
   constexpr int EPC = Vec<T>::EPC;
   constexpr int V = kRowBytes / (int)sizeof(T);  // cells per tile
@@ -263,12 +269,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(tail);
   double* sS = reinterpret_cast<double*>(tail + 128);  // [2][V]
   double* sW = sS + 2 * V;                              // [2][V]
-  double* red = sW + 2 * V;                             // [2][kWarps][V]
-  unsigned* s_ticket = reinterpret_cast<unsigned*>(red + 2 * kWarps * V);
+  double* red = sW + 2 * V;                             // [2][kRowsWarps][V]
+  unsigned* s_ticket = reinterpret_cast<unsigned*>(red + 2 * kRowsWarps * V);
   double* s_col = reinterpret_cast<double*>(s_ticket + 2);
   uint64_t* xbar = reinterpret_cast<uint64_t*>(tail + 64);        // [4] (CL)
   const uint32_t xoff =
-      ((smem_u32(s_col + kWarps) + 15u) & ~15u) - smem_u32(smem_raw);  // 16-B aligned
+      ((smem_u32(s_col + kRowsWarps) + 15u) & ~15u) - smem_u32(smem_raw);  // 16-B aligned
   double* xbuf = reinterpret_cast<double*>(smem_raw + xoff);        // [4][cs][V] (CL)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -311,10 +317,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // measured faster than one bulk copy per peer)
   auto send = [&](const double* rd, int64_t j) {
     const int slot = (int)(j & 3);
-    for (int v = tid; v < V / 2; v += kThreads) {
+    for (int v = tid; v < V / 2; v += kRowsThreads) {
       double a = 0.0, b = 0.0;
 #pragma unroll
-      for (int k = 0; k < kWarps; ++k) {
+      for (int k = 0; k < kRowsWarps; ++k) {
         a += rd[k * V + 2 * v];
         b += rd[k * V + 2 * v + 1];
       }
@@ -365,8 +371,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const unsigned char* base = st + p2_off;
 #define PIDB_ROWS_LOOP(BODY)                                                \
   _Pragma("unroll") for (int k = 0; k < ROWS; ++k) {                        \
-    if (k < ROWS - 1 || warp + k * kWarps < nloc) {                         \
-      const unsigned char* a = base + k * (kWarps * kRowBytes);             \
+    if (k < ROWS - 1 || warp + k * kRowsWarps < nloc) {                         \
+      const unsigned char* a = base + k * (kRowsWarps * kRowBytes);             \
       double v[EPL];                                                        \
       if constexpr (sizeof(T) == 4) {                                       \
         const float2 f = *reinterpret_cast<const float2*>(a);              \
@@ -393,12 +399,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #undef PIDB_ROWS_LOOP
   };
 
-  ColSweep<T> csw;
+  ColSweep<T, kRowsThreads> csw;
   int s_cur = 0, s_prev = 0;
   uint32_t par = 0;
   for (int64_t j = 0; j <= my_tiles; ++j) {
     const bool have = j < my_tiles;
-    double* rd = red + (j & 1) * kWarps * V;
+    double* rd = red + (j & 1) * kRowsWarps * V;
     if (have) {
       mbar_wait(&full[s_cur], par);
       if (mode != MODE_MASS) {
@@ -422,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_expect_tx(&xbar[(j - 2) & 3], xbytes);
       if (have) send(rd, j);
     } else if (have) {
-      finalize_tile<V, 0>(p, rd, (cid + j * ncl) * (int64_t)V, sS + (j & 1) * V,
+      finalize_tile<V, 0, kRowsThreads>(p, rd, (cid + j * ncl) * (int64_t)V, sS + (j & 1) * V,
                        sW + (j & 1) * V, mode != MODE_MASS, col_acc);
     }
     if (j >= 1) pass2(tiles + (size_t)s_prev * p.stage_bytes, (int)((j - 1) & 1), j - 1);
@@ -433,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // rows -> global partials (part layout [grid][n][2])
 #pragma unroll
   for (int k = 0; k < ROWS; ++k) {
-    const int rl = warp + k * kWarps;
+    const int rl = warp + k * kRowsWarps;
     const double a = warp_sum(acc_row[k]);
     const double b = warp_sum(acc_mass[k]);
     int nb = acc_nb[k];
@@ -448,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   if constexpr (CL) cluster_sync();  // no CTA leaves while peers may still target its SMEM
-  finish_partials(p, 1, col_acc, s_ticket, s_col);
+  finish_partials<kRowsThreads>(p, 1, col_acc, s_ticket, s_col);
 }
 
 // ---------------------------------------------------------------------------
@@ -691,7 +697,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  finish_partials(p, 2, col_acc, s_ticket, s_col);
+  finish_partials<kThreads>(p, 2, col_acc, s_ticket, s_col);
 }
 
 // ---------------------------------------------------------------- host side
@@ -709,7 +715,7 @@ struct Plan {
 };
 
 size_t rows_tail(int V, int cs) {
-  return 128 + (size_t)4 * V * 8 + (size_t)2 * kWarps * V * 8 + 16 + kWarps * 8 + 64 +
+  return 128 + (size_t)4 * V * 8 + (size_t)2 * kRowsWarps * V * 8 + 16 + kRowsWarps * 8 + 64 +
          (cs > 1 ? (size_t)4 * cs * V * 8 + 16 : 0);
 }
 
@@ -748,7 +754,7 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
       pl.grid = (int)std::max<int64_t>(
           cs, std::min<int64_t>(pl.tiles * cs, sm_count()) / cs * cs);
       pl.rpc = (int)((n + cs - 1) / cs);
-      pl.rows = (pl.rpc + kWarps - 1) / kWarps;
+      pl.rows = (pl.rpc + kRowsWarps - 1) / kRowsWarps;
       pl.box_rows = pl.rpc;
       pl.stage_bytes = (uint32_t)align_up((size_t)pl.rpc * kRowBytes, 1024);
       const size_t tb = rows_tail(V, cs) + 1024;
@@ -763,7 +769,7 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
   }
   if (n <= 256) {
     pl.chunked = false;
-    pl.rows = (int)((n + kWarps - 1) / kWarps);
+    pl.rows = (int)((n + kRowsWarps - 1) / kRowsWarps);
     pl.box_rows = (int)n;
     pl.stage_bytes = (uint32_t)align_up((size_t)n * kRowBytes, 1024);
     const size_t tb = rows_tail(V, 1) + 1024;
@@ -793,7 +799,7 @@ size_t workspace_bytes(const Plan& pl, int64_t n) {
 template <typename K>
 int launch(K kern, const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream_t st) {
   PIDB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-  kern<<<pl.grid, kThreads, pl.smem, st>>>(tm, sp);
+  kern<<<pl.grid, pl.chunked ? kThreads : kRowsThreads, pl.smem, st>>>(tm, sp);
   PIDB_LAUNCH_CHECK("stream kernel");
   return PIDB_OK;
 }
@@ -810,7 +816,7 @@ int launch_cluster(K kern, const CUtensorMap& tm, StreamParams& sp, const Plan& 
   attr[0].val.clusterDim.x = (unsigned)pl.cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kRowsThreads);
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = st;
   cfg.attrs = attr;
