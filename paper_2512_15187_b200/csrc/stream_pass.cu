@@ -458,6 +458,169 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// rows_ws_kernel: warp-specialised variant of rows_kernel for fp32, n <= 256.
+// Warps 0-3 (column group) run pass 1 and the S finalisation of tile j while
+// warps 4-15 (row group) run pass 2 of an earlier tile; the groups hand S over
+// through double-buffered sS/sW and named barriers (no CTA-wide barrier per
+// tile).  ROWS = ceil(n / 12) rows per row warp; MODE is a template argument
+// so only the accumulators of that mode are live.
+// Column-group size per mode: pass 1 is cheap packed-fp32 Fast2Sum for the
+// mean (S) and costs an fp64 conversion + FMA per element for T (MODE_COLS).
+__host__ __device__ constexpr int ws_col_warps(int mode) { return mode == MODE_COLS ? 8 : 4; }
+constexpr int kBarCols = 1, kBarSReady = 2, kBarSFree = 4, kBarRows = 6;  // named barriers
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <int ROWS, int MODE>
+__global__ void __launch_bounds__(kRowsThreads, 1)
+    rows_ws_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
+  using T = float;
+  constexpr int kWsColWarps = ws_col_warps(MODE);
+  constexpr int kWsColThreads = kWsColWarps * 32;
+  constexpr int kWsRowWarps = kRowsWarps - kWsColWarps;
+  constexpr int kWsRowThreads = kWsRowWarps * 32;
+  constexpr int EPC = Vec<T>::EPC;
+  constexpr int V = kRowBytes / (int)sizeof(T);
+  constexpr int EPL = 8 / (int)sizeof(T);
+  constexpr int kAll = kWsColThreads + kWsRowThreads;
+  constexpr int SWEEP = MODE == MODE_SIM ? MODE_MEAN : MODE;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  unsigned char* tiles = smem_raw + pad;
+  unsigned char* tail = tiles + (size_t)p.stages * p.stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tail);
+  double* sS = reinterpret_cast<double*>(tail + 128);  // [2][V]
+  double* sW = sS + 2 * V;                              // [2][V]
+  double* red = sW + 2 * V;                             // [kWsColWarps][V]
+  unsigned* s_ticket = reinterpret_cast<unsigned*>(red + kWsColWarps * V);
+  double* s_col = reinterpret_cast<double*>(s_ticket + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = (int)p.n;
+  const int G = gridDim.x;
+  const bool weighted = p.w != nullptr;
+  const int64_t my_tiles = p.tiles > blockIdx.x ? (p.tiles - 1 - blockIdx.x) / G + 1 : 0;
+  const uint64_t pol = policy_evict_first();
+
+  if (tid == 0) {
+    prefetch_tma_desc(&tmap);
+    for (int s = 0; s < p.stages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int64_t j) {
+    const int s = (int)(j % p.stages);
+    mbar_arrive_expect_tx(&full[s], (uint32_t)n * kRowBytes);
+    tma_load_2d(tiles + (size_t)s * p.stage_bytes, &tmap, (int32_t)((blockIdx.x + j * G) * V), 0,
+                &full[s], pol);
+  };
+  if (tid == 0)
+    for (int64_t j = 0; j < my_tiles && j < p.stages; ++j) issue(j);
+
+  double col_acc = 0.0;
+  double acc_row[ROWS], acc_mass[ROWS];
+#pragma unroll
+  for (int k = 0; k < ROWS; ++k) { acc_row[k] = 0.0; acc_mass[k] = 0.0; }
+
+  if (warp < kWsColWarps) {
+    // ---------------------------------------------------------- column group
+    const int q = tid & (kChunks16 - 1), ph = tid / kChunks16;
+    const uint32_t p1_off = (uint32_t)(ph * kRowBytes + q * 16);
+    ColSweep<T, kWsColThreads> csw;
+    int s = 0;
+    uint32_t par = 0;
+    for (int64_t j = 0; j < my_tiles; ++j) {
+      const int b = (int)(j & 1);
+      mbar_wait(&full[s], par);
+      csw.reset();
+      csw.run(tiles + (size_t)s * p.stage_bytes + p1_off, ph, n, SWEEP, p.inv, ph, n);
+      csw.combine(SWEEP);
+      if (lane < 16) {
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) red[warp * V + q * EPC + e] = csw.part[e];
+      }
+      named_sync(kBarCols, kWsColThreads);
+      double S = 0.0, wx = 0.0;
+      if (tid < V) {
+#pragma unroll
+        for (int k = 0; k < kWsColWarps; ++k) S += red[k * V + tid];
+        const int64_t x = (blockIdx.x + j * G) * (int64_t)V + tid;
+        wx = x < p.m ? (weighted ? __ldg(p.w + x) : 1.0) : 0.0;
+      }
+      named_sync(kBarSFree + b, kAll);  // the row group is done with sS/sW[b]
+      if (tid < V) {
+        sW[b * V + tid] = wx;
+        sS[b * V + tid] = MODE == MODE_SIM ? __ddiv_rn(S, (double)p.n) : wx * S;
+        col_acc = fma(wx, S, col_acc);
+      }
+      named_arrive(kBarSReady + b, kAll);
+      if (++s == p.stages) { s = 0; par ^= 1u; }
+    }
+  } else {
+    // ------------------------------------------------------------- row group
+    const int rw = warp - kWsColWarps;
+    const uint32_t p2_off = (uint32_t)(rw * kRowBytes + lane * 8);
+    const int cell = lane * EPL;
+    named_arrive(kBarSFree + 0, kAll);  // both S buffers start free
+    named_arrive(kBarSFree + 1, kAll);
+    int s = 0;
+    for (int64_t j = 0; j < my_tiles; ++j) {
+      const int b = (int)(j & 1);
+      named_sync(kBarSReady + b, kAll);
+      double s_l[EPL], w_l[EPL];
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        s_l[e] = sS[b * V + cell + e];
+        w_l[e] = sW[b * V + cell + e];
+      }
+      named_arrive(kBarSFree + b, kAll);
+      const unsigned char* base = tiles + (size_t)s * p.stage_bytes + p2_off;
+#pragma unroll
+      for (int k = 0; k < ROWS; ++k) {
+        if (k < ROWS - 1 || rw + k * kWsRowWarps < n) {
+          const float2 f = *reinterpret_cast<const float2*>(base + k * (kWsRowWarps * kRowBytes));
+          const double v[2] = {f.x, f.y};
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) {
+            if (MODE == MODE_SIM) {
+              acc_row[k] = fma(fmin(v[e], s_l[e]), w_l[e], acc_row[k]);
+              acc_mass[k] = fma(v[e], w_l[e], acc_mass[k]);
+            } else if (MODE == MODE_COLS) {
+              acc_row[k] = fma(v[e], s_l[e], acc_row[k]);
+            } else {
+              acc_row[k] = fma(v[e], s_l[e], acc_row[k]);
+              acc_mass[k] = weighted ? fma(v[e], w_l[e], acc_mass[k]) : acc_mass[k] + v[e];
+            }
+          }
+        }
+      }
+      named_sync(kBarRows, kWsRowThreads);  // every row warp is done with stage s
+      if (rw == 0 && lane == 0 && j + p.stages < my_tiles) issue(j + p.stages);
+      if (++s == p.stages) s = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < ROWS; ++k) {
+      const int r = rw + k * kWsRowWarps;
+      const double a = warp_sum(acc_row[k]);
+      const double c = warp_sum(acc_mass[k]);
+      if (lane == 0 && r < n) {
+        double* dst = p.part + ((size_t)blockIdx.x * n + r) * 2;
+        dst[0] = a;
+        dst[1] = c;
+      }
+    }
+  }
+  __syncthreads();
+  finish_partials<kRowsThreads>(p, 1, col_acc, s_ticket, s_col);
+}
+
+// ---------------------------------------------------------------------------
 // chunked_kernel: 256 < n <= 256 * CMAX.  Thread t owns half (t >> 8) of row
 // (t & 255) of every chunk; it reads the half's 8 chunks in a row-rotated
 // order (bank-conflict free without swizzle) and keeps its row sums for chunk
@@ -855,6 +1018,34 @@ int launch_typed(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaSt
     return PIDB_EUNSUPPORTED;
   }
   sp.groups = pl.grid;
+  if constexpr (sizeof(T) == 4) {
+    // warp-specialised rows kernel (fp32, n <= 256, not the masses-only mode):
+    // 0.95 of HBM on cfg5 vs 0.84 for rows_kernel; PIDB_WS=0 selects the latter
+    const char* e = std::getenv("PIDB_WS");
+    const bool ws = e == nullptr || e[0] != '0';
+    if (ws && !pl.chunked && pl.cs == 1 && sp.mode != MODE_MASS) {
+      const int rw = kRowsWarps - ws_col_warps(sp.mode);
+      const int rows = (int)((sp.n + rw - 1) / rw);
+      switch (sp.mode * 32 + rows) {
+#define PIDB_WS_CASE(M, R) \
+  case M * 32 + R: return launch(rows_ws_kernel<R, M>, tm, sp, pl, st);
+#define PIDB_WS_MODE(M)                                                                   \
+  PIDB_WS_CASE(M, 1) PIDB_WS_CASE(M, 2) PIDB_WS_CASE(M, 3) PIDB_WS_CASE(M, 4)             \
+  PIDB_WS_CASE(M, 5) PIDB_WS_CASE(M, 6) PIDB_WS_CASE(M, 7) PIDB_WS_CASE(M, 8)             \
+  PIDB_WS_CASE(M, 9) PIDB_WS_CASE(M, 10) PIDB_WS_CASE(M, 11) PIDB_WS_CASE(M, 12)          \
+  PIDB_WS_CASE(M, 13) PIDB_WS_CASE(M, 14) PIDB_WS_CASE(M, 15) PIDB_WS_CASE(M, 16)         \
+  PIDB_WS_CASE(M, 17) PIDB_WS_CASE(M, 18) PIDB_WS_CASE(M, 19) PIDB_WS_CASE(M, 20)         \
+  PIDB_WS_CASE(M, 21) PIDB_WS_CASE(M, 22)
+        PIDB_WS_MODE(0) PIDB_WS_MODE(1) PIDB_WS_MODE(3)
+        PIDB_WS_CASE(1, 23) PIDB_WS_CASE(1, 24) PIDB_WS_CASE(1, 25) PIDB_WS_CASE(1, 26)
+        PIDB_WS_CASE(1, 27) PIDB_WS_CASE(1, 28) PIDB_WS_CASE(1, 29) PIDB_WS_CASE(1, 30)
+        PIDB_WS_CASE(1, 31) PIDB_WS_CASE(1, 32)
+#undef PIDB_WS_MODE
+#undef PIDB_WS_CASE
+        default: break;
+      }
+    }
+  }
   if (pl.chunked) {
     const int C = (int)((sp.n + kChunkRows - 1) / kChunkRows);
     if (C <= 4) return launch(chunked_kernel<T, 4>, tm, sp, pl, st);
