@@ -476,7 +476,7 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <int ROWS, int MODE>
+template <int ROWS, int MODE, bool CL>
 __global__ void __launch_bounds__(kRowsThreads, 1)
     rows_ws_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
   using T = float;
@@ -495,29 +495,44 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   unsigned char* tiles = smem_raw + pad;
   unsigned char* tail = tiles + (size_t)p.stages * p.stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(tail);
-  double* sS = reinterpret_cast<double*>(tail + 128);  // [2][V]
-  double* sW = sS + 2 * V;                              // [2][V]
-  double* red = sW + 2 * V;                             // [kWsColWarps][V]
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(tail + 64);  // [4] (CL)
+  double* sS = reinterpret_cast<double*>(tail + 128);       // [2][V]
+  double* sW = sS + 2 * V;                                   // [2][V]
+  double* red = sW + 2 * V;                                  // [kWsColWarps][V]
   unsigned* s_ticket = reinterpret_cast<unsigned*>(red + kWsColWarps * V);
   double* s_col = reinterpret_cast<double*>(s_ticket + 2);
+  const uint32_t xoff =
+      ((smem_u32(s_col + kRowsWarps) + 15u) & ~15u) - smem_u32(smem_raw);
+  double* xbuf = reinterpret_cast<double*>(smem_raw + xoff);  // [4][cs][V] (CL)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = (int)p.n;
-  const int G = gridDim.x;
   const bool weighted = p.w != nullptr;
-  const int64_t my_tiles = p.tiles > blockIdx.x ? (p.tiles - 1 - blockIdx.x) / G + 1 : 0;
+  const int cs = CL ? p.cs : 1;
+  const uint32_t rank = CL ? cluster_rank() : 0u;
+  const int cid = (int)blockIdx.x / cs, ncl = (int)gridDim.x / cs;
+  const int r0 = CL ? (int)rank * p.rpc : 0;
+  const int box = CL ? p.rpc : n;                        // member rows per TMA box
+  const int nloc = CL ? max(0, min(n - r0, p.rpc)) : n;  // member rows of this CTA
+  const int64_t my_tiles = p.tiles > cid ? (p.tiles - 1 - cid) / ncl + 1 : 0;
   const uint64_t pol = policy_evict_first();
+  const uint32_t xbytes = (uint32_t)cs * V * 8u;
 
   if (tid == 0) {
     prefetch_tma_desc(&tmap);
     for (int s = 0; s < p.stages; ++s) mbar_init(&full[s], 1);
+    if (CL)
+      for (int s = 0; s < 4; ++s) mbar_init(&xbar[s], 1);
     fence_mbar_init();
+    if (CL)
+      for (int s = 0; s < 4 && s < my_tiles; ++s) mbar_arrive_expect_tx(&xbar[s], xbytes);
   }
   __syncthreads();
+  if constexpr (CL) cluster_sync();  // peers' mbarriers exist before any st.async
   auto issue = [&](int64_t j) {
     const int s = (int)(j % p.stages);
-    mbar_arrive_expect_tx(&full[s], (uint32_t)n * kRowBytes);
-    tma_load_2d(tiles + (size_t)s * p.stage_bytes, &tmap, (int32_t)((blockIdx.x + j * G) * V), 0,
+    mbar_arrive_expect_tx(&full[s], (uint32_t)box * kRowBytes);
+    tma_load_2d(tiles + (size_t)s * p.stage_bytes, &tmap, (int32_t)((cid + j * ncl) * V), r0,
                 &full[s], pol);
   };
   if (tid == 0)
@@ -537,27 +552,45 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     uint32_t par = 0;
     for (int64_t j = 0; j < my_tiles; ++j) {
       const int b = (int)(j & 1);
+      const int64_t x0 = (cid + j * ncl) * (int64_t)V;
+      double wx = 0.0;
+      if (tid < V) {
+        const int64_t x = x0 + tid;
+        wx = x < p.m ? (weighted ? __ldg(p.w + x) : 1.0) : 0.0;
+      }
       mbar_wait(&full[s], par);
       csw.reset();
-      csw.run(tiles + (size_t)s * p.stage_bytes + p1_off, ph, n, SWEEP, p.inv, ph, n);
+      csw.run(tiles + (size_t)s * p.stage_bytes + p1_off, ph, box, SWEEP, p.inv, r0 + ph, n);
       csw.combine(SWEEP);
       if (lane < 16) {
 #pragma unroll
         for (int e = 0; e < EPC; ++e) red[warp * V + q * EPC + e] = csw.part[e];
       }
       named_sync(kBarCols, kWsColThreads);
-      double S = 0.0, wx = 0.0;
+      double S = 0.0;
       if (tid < V) {
 #pragma unroll
         for (int k = 0; k < kWsColWarps; ++k) S += red[k * V + tid];
-        const int64_t x = (blockIdx.x + j * G) * (int64_t)V + tid;
-        wx = x < p.m ? (weighted ? __ldg(p.w + x) : 1.0) : 0.0;
       }
-      named_sync(kBarSFree + b, kAll);  // the row group is done with sS/sW[b]
-      if (tid < V) {
-        sW[b * V + tid] = wx;
-        sS[b * V + tid] = MODE == MODE_SIM ? __ddiv_rn(S, (double)p.n) : wx * S;
-        col_acc = fma(wx, S, col_acc);
+      // the row group has read sS/sW[b] (and, CL, xbuf slot of tile j-2)
+      named_sync(kBarSFree + b, kAll);
+      if constexpr (CL) {
+        // CTA partial of column S -> every CTA of the cluster (16-byte st.async
+        // completing on the receiver's mbarrier); rank order is kept by slot
+        const double S1 = __shfl_down_sync(0xffffffffu, S, 1);
+        if (tid < V && (tid & 1) == 0) {
+          const int slot = (int)(j & 3);
+          const uint32_t la = smem_u32(xbuf + ((size_t)slot * cs + rank) * V + tid);
+          const uint32_t lb = smem_u32(&xbar[slot]);
+          for (int c = 0; c < cs; ++c) st_async_f64x2(mapa(la, c), S, S1, mapa(lb, c));
+        }
+        if (tid < V) sW[b * V + tid] = wx;
+      } else {
+        if (tid < V) {
+          sW[b * V + tid] = wx;
+          sS[b * V + tid] = MODE == MODE_SIM ? __ddiv_rn(S, (double)p.n) : wx * S;
+          col_acc = fma(wx, S, col_acc);
+        }
       }
       named_arrive(kBarSReady + b, kAll);
       if (++s == p.stages) { s = 0; par ^= 1u; }
@@ -574,16 +607,29 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       const int b = (int)(j & 1);
       named_sync(kBarSReady + b, kAll);
       double s_l[EPL], w_l[EPL];
+      if constexpr (CL) {
+        const int slot = (int)(j & 3);
+        mbar_wait(&xbar[slot], (uint32_t)((j >> 2) & 1));
 #pragma unroll
-      for (int e = 0; e < EPL; ++e) {
-        s_l[e] = sS[b * V + cell + e];
-        w_l[e] = sW[b * V + cell + e];
+        for (int e = 0; e < EPL; ++e) {
+          double S = 0.0;
+          for (int c = 0; c < cs; ++c) S += xbuf[((size_t)slot * cs + c) * V + cell + e];
+          w_l[e] = sW[b * V + cell + e];
+          s_l[e] = MODE == MODE_SIM ? __ddiv_rn(S, (double)p.n) : w_l[e] * S;
+          if (rank == 0 && rw == 0) col_acc = fma(w_l[e], S, col_acc);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          s_l[e] = sS[b * V + cell + e];
+          w_l[e] = sW[b * V + cell + e];
+        }
       }
       named_arrive(kBarSFree + b, kAll);
       const unsigned char* base = tiles + (size_t)s * p.stage_bytes + p2_off;
 #pragma unroll
       for (int k = 0; k < ROWS; ++k) {
-        if (k < ROWS - 1 || rw + k * kWsRowWarps < n) {
+        if (k < ROWS - 1 || rw + k * kWsRowWarps < nloc) {
           const float2 f = *reinterpret_cast<const float2*>(base + k * (kWsRowWarps * kRowBytes));
           const double v[2] = {f.x, f.y};
 #pragma unroll
@@ -601,22 +647,27 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         }
       }
       named_sync(kBarRows, kWsRowThreads);  // every row warp is done with stage s
-      if (rw == 0 && lane == 0 && j + p.stages < my_tiles) issue(j + p.stages);
+      if (rw == 0 && lane == 0) {
+        if (j + p.stages < my_tiles) issue(j + p.stages);
+        // every row thread passed its xbar wait for tile j: re-arm for tile j+4
+        if (CL && j + 4 < my_tiles) mbar_arrive_expect_tx(&xbar[j & 3], xbytes);
+      }
       if (++s == p.stages) s = 0;
     }
 #pragma unroll
     for (int k = 0; k < ROWS; ++k) {
-      const int r = rw + k * kWsRowWarps;
+      const int rl = rw + k * kWsRowWarps;
       const double a = warp_sum(acc_row[k]);
       const double c = warp_sum(acc_mass[k]);
-      if (lane == 0 && r < n) {
-        double* dst = p.part + ((size_t)blockIdx.x * n + r) * 2;
+      if (lane == 0 && rl < nloc) {
+        double* dst = p.part + ((size_t)cid * n + r0 + rl) * 2;
         dst[0] = a;
         dst[1] = c;
       }
     }
   }
   __syncthreads();
+  if constexpr (CL) cluster_sync();  // no CTA leaves while peers may still target its SMEM
   finish_partials<kRowsThreads>(p, 1, col_acc, s_ticket, s_col);
 }
 
@@ -886,9 +937,10 @@ size_t rows_tail(int V, int cs) {
 // (tools/prof_k5.py, 256^3 cells): pairs of CTAs win for
 // n <= 512 and 8-CTA clusters for 1536 < n <= 2048; in between the chunked
 // kernel is faster.  PIDB_CLUSTER overrides (tuning).
-int cluster_size_for(int64_t n) {
+int cluster_size_for(int64_t n, bool ws) {
   int cs = 0;
-  if (n <= 512) cs = 2;
+  if (ws) cs = n <= 2048 ? (int)((n + 255) / 256) : 0;  // warp-specialised: <= 256 rows per CTA
+  else if (n <= 512) cs = 2;
   else if (n > 1536 && n <= 2048) cs = 8;
   if (const char* e = std::getenv("PIDB_CLUSTER")) {
     const int v = std::atoi(e);
@@ -902,7 +954,9 @@ size_t chunked_smem(int V) {
          kWarps * 8 + 64;
 }
 
-bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
+bool ws_eligible(int esize, int mode) { return esize == 4 && mode != MODE_MASS; }
+
+bool make_plan(int64_t n, int64_t m, int esize, Plan& pl, int mode = MODE_MEAN) {
   if (n < 1 || m < 1) return false;
   const int V = kRowBytes / esize;
   pl.tiles = (m + V - 1) / V;
@@ -910,7 +964,7 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl) {
   pl.cs = 1;
   pl.rpc = (int)n;
   if (n > 256 && n <= 16 * 256) {
-    const int cs = cluster_size_for(n);
+    const int cs = cluster_size_for(n, ws_eligible(esize, mode) && std::getenv("PIDB_WS") == nullptr);
     if (cs >= 2 && cs <= 16) {
       pl.chunked = false;
       pl.cs = cs;
@@ -1004,6 +1058,30 @@ int launch_cluster(K kern, const CUtensorMap& tm, StreamParams& sp, const Plan& 
 
 template <typename T>
 int launch_typed(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4) {
+    if (pl.cs > 1 && ws_eligible(4, sp.mode) && std::getenv("PIDB_WS") == nullptr) {
+      const int rw = kRowsWarps - ws_col_warps(sp.mode);
+      const int rows = (pl.rpc + rw - 1) / rw;
+      switch (sp.mode * 64 + rows) {
+#define PIDB_WSC_CASE(M, R) \
+  case M * 64 + R: return launch_cluster(rows_ws_kernel<R, M, true>, tm, sp, pl, st);
+#define PIDB_WSC_MODE(M)                                                                    \
+  PIDB_WSC_CASE(M, 1) PIDB_WSC_CASE(M, 2) PIDB_WSC_CASE(M, 3) PIDB_WSC_CASE(M, 4)           \
+  PIDB_WSC_CASE(M, 5) PIDB_WSC_CASE(M, 6) PIDB_WSC_CASE(M, 7) PIDB_WSC_CASE(M, 8)           \
+  PIDB_WSC_CASE(M, 9) PIDB_WSC_CASE(M, 10) PIDB_WSC_CASE(M, 11) PIDB_WSC_CASE(M, 12)        \
+  PIDB_WSC_CASE(M, 13) PIDB_WSC_CASE(M, 14) PIDB_WSC_CASE(M, 15) PIDB_WSC_CASE(M, 16)       \
+  PIDB_WSC_CASE(M, 17) PIDB_WSC_CASE(M, 18) PIDB_WSC_CASE(M, 19) PIDB_WSC_CASE(M, 20)       \
+  PIDB_WSC_CASE(M, 21) PIDB_WSC_CASE(M, 22)
+        PIDB_WSC_MODE(0) PIDB_WSC_MODE(1) PIDB_WSC_MODE(3)
+        PIDB_WSC_CASE(1, 23) PIDB_WSC_CASE(1, 24) PIDB_WSC_CASE(1, 25) PIDB_WSC_CASE(1, 26)
+        PIDB_WSC_CASE(1, 27) PIDB_WSC_CASE(1, 28) PIDB_WSC_CASE(1, 29) PIDB_WSC_CASE(1, 30)
+        PIDB_WSC_CASE(1, 31) PIDB_WSC_CASE(1, 32)
+#undef PIDB_WSC_MODE
+#undef PIDB_WSC_CASE
+        default: break;
+      }
+    }
+  }
   if (pl.cs > 1) {
     switch (pl.rows) {
 #define PIDB_CL_CASE(R) \
@@ -1021,14 +1099,13 @@ int launch_typed(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaSt
   if constexpr (sizeof(T) == 4) {
     // warp-specialised rows kernel (fp32, n <= 256, not the masses-only mode):
     // 0.95 of HBM on cfg5 vs 0.84 for rows_kernel; PIDB_WS=0 selects the latter
-    const char* e = std::getenv("PIDB_WS");
-    const bool ws = e == nullptr || e[0] != '0';
+    const bool ws = std::getenv("PIDB_WS") == nullptr;  // PIDB_WS=<anything>: old kernels
     if (ws && !pl.chunked && pl.cs == 1 && sp.mode != MODE_MASS) {
       const int rw = kRowsWarps - ws_col_warps(sp.mode);
       const int rows = (int)((sp.n + rw - 1) / rw);
       switch (sp.mode * 32 + rows) {
 #define PIDB_WS_CASE(M, R) \
-  case M * 32 + R: return launch(rows_ws_kernel<R, M>, tm, sp, pl, st);
+  case M * 32 + R: return launch(rows_ws_kernel<R, M, false>, tm, sp, pl, st);
 #define PIDB_WS_MODE(M)                                                                   \
   PIDB_WS_CASE(M, 1) PIDB_WS_CASE(M, 2) PIDB_WS_CASE(M, 3) PIDB_WS_CASE(M, 4)             \
   PIDB_WS_CASE(M, 5) PIDB_WS_CASE(M, 6) PIDB_WS_CASE(M, 7) PIDB_WS_CASE(M, 8)             \
@@ -1077,7 +1154,7 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
                "row stride %lld must be >= m and a multiple of 16 bytes", (long long)ld);
   PIDB_REQUIRE((reinterpret_cast<uintptr_t>(u) & 15) == 0, "member matrix must be 16-byte aligned");
   Plan pl;
-  if (!make_plan(n, m, es, pl))
+  if (!make_plan(n, m, es, pl, mode))
     return run_wide_pass(mode, u, dtype, n, m, ld, w, inv, out_row, out_mass, out_col, out_nb, ws,
                          ws_bytes, stream);
   const size_t need = workspace_bytes(pl, n);
