@@ -23,7 +23,7 @@ def _dev_values(x, dev, dtype=None) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         t = x.reshape(-1)
     else:
-        t = torch.from_numpy(np.ascontiguousarray(np.asarray(x).reshape(-1)))
+        t = torch.from_numpy(np.array(np.asarray(x).reshape(-1)))  # writable copy
     if dtype is not None:
         t = t.to(dtype)
     elif t.dtype not in (torch.float32, torch.float64):

@@ -343,6 +343,7 @@ def test_errors_and_warning(pb):
     (1, (37,), False), (3, (5, 5), True), (33, (31, 7), False), (100, (64, 65), True),
     (257, (50, 21), False), (300, (40, 40), True), (700, (33, 35), False),
     (1000, (16, 16, 16), True), (1500, (24, 24), False), (2000, (17, 19), True),
+    (2600, (9, 70), True), (3500, (33,), False), (4096, (11, 13), True),
 ])
 def test_layouts_vs_oracle(pb, n, dims, weighted):
     U, w = make_fuzzy(1000 + n, n, dims, weighted)
