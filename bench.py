@@ -339,6 +339,12 @@ def run_ours(args, rank, world, local, pg):
                      "frac": achieved / pk["hbm_gbs"] if achieved else None,
                      "traffic": ncu_traffic(args.workload, world),
                      "algorithmic_bytes_per_launch": alg_bytes,
+                     # the peak above is a copy (read + write) benchmark; a pure
+                     # read stream goes faster: our TMA streaming microbenchmark
+                     # (tools/ubench_tma.cu, profiles/r01_ubench_tma.log) reached
+                     # 7227 GB/s with 512-byte box rows
+                     "read_stream_peak": READ_STREAM_PEAK_GBS,
+                     "frac_read_stream": achieved / READ_STREAM_PEAK_GBS if achieved else None,
                      "kernel_ms": kms, "launches_timed": klaunch, "peak_src": pk["src"]},
         "gpu_launches": launches_per_step * args.steps,
         "min_depth_gap": float(np.min(np.diff(np.sort(res_chk.depth)))) if n > 1 else None,
@@ -425,6 +431,7 @@ def run_e2e(args, host, _, meta, fn, world, pg, dev):
 # cuBLAS TF32 / INT8 dense GEMM peaks measured on this pool's B200 by
 # tools/probe_box.sh (8192^3, best of 20; profiles/r01_probe_box.log).
 TF32_TFLOPS_PROBE = 747.2
+READ_STREAM_PEAK_GBS = 7227.4  # TMA 2D read stream, 512-B rows (profiles/r01_ubench_tma.log)
 INT8_TOPS_PROBE = 3004.5
 
 
