@@ -219,8 +219,8 @@ def member_masses(ensemble, workers: int | None = None, require_binary: bool = F
 
 
 def _raise_first_nonbinary(de: DeviceEnsemble, nb: torch.Tensor) -> None:
-    bad = torch.nonzero(nb).flatten()
-    if bad.numel():
+    bad = np.flatnonzero(nb.cpu().numpy())
+    if bad.size:
         i = int(bad[0])
         raise ValidationError(f"member {de.ids[i]!r} is not binary (0/1) valued")
 
@@ -336,11 +336,13 @@ def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
         nb = torch.zeros(n, dtype=torch.int64, device=dev)
         packed = pack_binary(de, nb)
         _allreduce(nb, de)
-        _raise_first_nonbinary(de, nb)
         g = intersection_gram(de, packed)
         mslot, ii, io, d = out.ptrs()
         N.call("pidb_eid_exact_epilogue", g.data_ptr(), n, ii, io, d, out.rank.data_ptr(),
                mslot, stream_ptr(dev))
+        # one host round trip: the non-binary check is read after the whole
+        # stream has been queued (the results are discarded if it fails)
+        _raise_first_nonbinary(de, nb)
         masses = out.vals[:n].cpu().numpy()
     else:
         mass, nb = _masses_device(de, with_nonbinary=True)
