@@ -118,9 +118,16 @@ def dist_setup():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("PIDB_BENCH_SHARE_GPU") == "1":
+            # flow check only (tools/dist_check.sh): every rank on cuda:0, gloo
+            # collectives; the timings of such a run mean nothing
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist.group.WORLD
     return rank, world, local, pg
 
