@@ -627,16 +627,22 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       }
       named_arrive(kBarSFree + b, kAll);
       const unsigned char* base = tiles + (size_t)s * p.stage_bytes + p2_off;
+      // SIM: min(u, mean) with u fp32 decided in fp32 (u <= mean exactly when
+      // u <= the largest float <= mean), saving the fp64 min per element
+      float md[EPL];
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) md[e] = MODE == MODE_SIM ? __double2float_rd(s_l[e]) : 0.f;
 #pragma unroll
       for (int k = 0; k < ROWS; ++k) {
         if (k < ROWS - 1 || rw + k * kWsRowWarps < nloc) {
           const float2 f = *reinterpret_cast<const float2*>(base + k * (kWsRowWarps * kRowBytes));
+          const float fv[2] = {f.x, f.y};
           const double v[2] = {f.x, f.y};
 #pragma unroll
           for (int e = 0; e < EPL; ++e) {
             if (MODE == MODE_SIM) {
-              acc_row[k] = fma(fmin(v[e], s_l[e]), w_l[e], acc_row[k]);
-              acc_mass[k] = fma(v[e], w_l[e], acc_mass[k]);
+              acc_row[k] = fma(fv[e] <= md[e] ? v[e] : s_l[e], w_l[e], acc_row[k]);
+              acc_mass[k] = weighted ? fma(v[e], w_l[e], acc_mass[k]) : acc_mass[k] + v[e];
             } else if (MODE == MODE_COLS) {
               acc_row[k] = fma(v[e], s_l[e], acc_row[k]);
             } else {
