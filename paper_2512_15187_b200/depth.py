@@ -120,6 +120,36 @@ def _launch(name: str, *args) -> None:
 
 
 
+# CUDA graphs for repeated calls on one DeviceEnsemble (PIDB_GRAPHS=0: off)
+_GRAPHS = os.environ.get("PIDB_GRAPHS", "1") != "0"
+
+
+def _graphed(de: DeviceEnsemble, key: str, enqueue):
+    """Queue the device work of one call; returns enqueue()'s output tensors.
+
+    A DeviceEnsemble reused for the same method runs eagerly once (plans,
+    workspaces), is captured into a CUDA graph on its second call and
+    replayed afterwards: one graph launch instead of the ctypes launches and
+    allocations of the eager path (the small configurations are
+    launch-bound).  Sharded ensembles (NCCL in the sequence) and timed runs
+    (KERNEL_EVENTS) stay eager."""
+    if not _GRAPHS or de.sharded or KERNEL_EVENTS is not None:
+        return enqueue()
+    cache = de._cache.setdefault("graphs", {})
+    ent = cache.get(key)
+    if ent is None:
+        cache[key] = False
+        return enqueue()
+    if ent is False:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            outs = enqueue()
+        ent = cache[key] = (g, outs)
+    g, outs = ent
+    g.replay()
+    return outs
+
+
 def _f64(n: int, dev) -> torch.Tensor:
     return torch.empty(n, dtype=torch.float64, device=dev)
 
@@ -183,16 +213,18 @@ class _Out:
 
     def __init__(self, n: int, dev):
         self.n = n
-        self.vals = _f64(4 * n, dev)
-        self.rank = torch.empty(n, dtype=torch.int64, device=dev)
+        self.block = _f64(5 * n, dev)  # one allocation -> one D2H
+        self.vals = self.block[:4 * n]
+        self.rank = self.block[4 * n:].view(torch.int64)
 
     def ptrs(self):
         p, n = self.vals.data_ptr(), self.n
         return p, p + 8 * n, p + 16 * n, p + 24 * n
 
     def fetch(self):
-        v = self.vals.cpu().numpy().reshape(4, self.n)
-        r = self.rank.cpu().numpy()
+        h = self.block.cpu().numpy()
+        v = h[:4 * self.n].reshape(4, self.n)
+        r = h[4 * self.n:].view(np.int64)
         return v[1].copy(), v[2].copy(), v[3].copy(), r.copy()
 
 
@@ -236,12 +268,17 @@ def depth_pid_mean(ensemble, workers: int | None = None,
     resolve_workers(workers)
     de = stage(ensemble)
     n, dev = de.n, de.device
-    buf = _mean_partials(de)
-    out = _Out(n, dev)
-    p = buf.data_ptr()
-    inv, ii, io, d = out.ptrs()
-    N.call("pidb_depth_epilogue", N.PIDB_EPI_PID_MEAN, n, p, p + 8 * n, p + 16 * n,
-           inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
+
+    def enqueue():
+        buf = _mean_partials(de)
+        out = _Out(n, dev)
+        p = buf.data_ptr()
+        inv, ii, io, d = out.ptrs()
+        N.call("pidb_depth_epilogue", N.PIDB_EPI_PID_MEAN, n, p, p + 8 * n, p + 16 * n,
+               inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
+        return buf, out
+
+    buf, out = _graphed(de, "pid-mean", enqueue)
     host = buf[n:].cpu().numpy()
     masses, col_mean = host[:n], float(host[n])
     if col_mean == 0.0:
@@ -257,9 +294,10 @@ def depth_pid_mean(ensemble, workers: int | None = None,
     return res
 
 
-def _pid_factorized(de: DeviceEnsemble, out: _Out) -> np.ndarray:
+def _pid_factorized(de: DeviceEnsemble, out: _Out) -> torch.Tensor:
     """Exact PID in two HBM passes: K5 gives row_plain and masses, K9-B the
-    inverse-mass-weighted column sums (SURVEY.md §0 finding 2)."""
+    inverse-mass-weighted column sums (SURVEY.md §0 finding 2).  Queues the
+    work and returns the K5 block [row_plain | mass | col]."""
     n, dev = de.n, de.device
     buf = _mean_partials(de)
     p = buf.data_ptr()
@@ -269,7 +307,7 @@ def _pid_factorized(de: DeviceEnsemble, out: _Out) -> np.ndarray:
     _, ii, io, d = out.ptrs()
     N.call("pidb_depth_epilogue", N.PIDB_EPI_PID, n, p, p + 8 * n, col.data_ptr(),
            inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
-    return buf[n:2 * n].cpu().numpy()
+    return buf
 
 
 def _pid_gram(de: DeviceEnsemble, out: _Out) -> np.ndarray:
@@ -310,9 +348,17 @@ def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") 
     if algorithm not in PID_ALGORITHMS:
         raise ValidationError(f"unknown pid algorithm {algorithm!r}; expected one of {PID_ALGORITHMS}")
     de = stage(ensemble)
-    out = _Out(de.n, de.device)
-    use_gram = algorithm == "gram"
-    masses = _pid_gram(de, out) if use_gram else _pid_factorized(de, out)
+    n = de.n
+    if algorithm == "gram":
+        out = _Out(n, de.device)
+        masses = _pid_gram(de, out)
+    else:
+        def enqueue():
+            out = _Out(n, de.device)
+            return _pid_factorized(de, out), out
+
+        buf, out = _graphed(de, "pid", enqueue)
+        masses = buf[n:2 * n].cpu().numpy()
     return _finish(de, out, "pid", masses, t0)
 
 
@@ -327,24 +373,29 @@ def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
     resolve_workers(workers)
     de = stage(ensemble)
     n, dev = de.n, de.device
-    out = _Out(n, dev)
     if de.weights is None:
         from .reduction import intersection_gram, pack_binary
 
-        # K7 packs and counts non-binary values in the same pass; the masses
-        # are the Gram diagonal |C_i| (exact integers)
-        nb = torch.zeros(n, dtype=torch.int64, device=dev)
-        packed = pack_binary(de, nb)
-        _allreduce(nb, de)
-        g = intersection_gram(de, packed)
-        mslot, ii, io, d = out.ptrs()
-        N.call("pidb_eid_exact_epilogue", g.data_ptr(), n, ii, io, d, out.rank.data_ptr(),
-               mslot, stream_ptr(dev))
+        def enqueue():
+            # K7 packs and counts non-binary values in the same pass; the
+            # masses are the Gram diagonal |C_i| (exact integers)
+            out = _Out(n, dev)
+            nb = torch.zeros(n, dtype=torch.int64, device=dev)
+            packed = pack_binary(de, nb)
+            _allreduce(nb, de)
+            g = intersection_gram(de, packed)
+            mslot, ii, io, d = out.ptrs()
+            N.call("pidb_eid_exact_epilogue", g.data_ptr(), n, ii, io, d, out.rank.data_ptr(),
+                   mslot, stream_ptr(dev))
+            return nb, out
+
+        nb, out = _graphed(de, "eid", enqueue)
         # one host round trip: the non-binary check is read after the whole
         # stream has been queued (the results are discarded if it fails)
         _raise_first_nonbinary(de, nb)
         masses = out.vals[:n].cpu().numpy()
     else:
+        out = _Out(n, dev)
         mass, nb = _masses_device(de, with_nonbinary=True)
         _raise_first_nonbinary(de, nb)
         buf = _mean_partials(de)
@@ -378,16 +429,22 @@ def depth_similarity_baseline(ensemble, measure: str, workers: int | None = None
     resolve_workers(workers)
     de = stage(ensemble)
     n, dev = de.n, de.device
-    buf = _f64(2 * n + 1, dev)
-    ws = de.workspace(N.load().pidb_pid_mean_workspace_bytes(de.n, de.m, de.dtype_code))
-    p = buf.data_ptr()
-    _launch("pidb_similarity_partials", de.ptr(), de.dtype_code, n, de.m, de.ld, de.wptr(),
-            p, p + 8 * n, p + 16 * n, ws.data_ptr(), ws.numel(), stream_ptr(dev))
-    _allreduce(buf, de)
-    out = _Out(n, dev)
-    inv, ii, io, d = out.ptrs()
-    N.call("pidb_depth_epilogue", N.PIDB_EPI_DICE if kind == "dice" else N.PIDB_EPI_IOU, n,
-           p, p + 8 * n, p + 16 * n, inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
+
+    def enqueue():
+        buf = _f64(2 * n + 1, dev)
+        ws = de.workspace(N.load().pidb_pid_mean_workspace_bytes(de.n, de.m, de.dtype_code))
+        p = buf.data_ptr()
+        _launch("pidb_similarity_partials", de.ptr(), de.dtype_code, n, de.m, de.ld, de.wptr(),
+                p, p + 8 * n, p + 16 * n, ws.data_ptr(), ws.numel(), stream_ptr(dev))
+        _allreduce(buf, de)
+        out = _Out(n, dev)
+        inv, ii, io, d = out.ptrs()
+        N.call("pidb_depth_epilogue", N.PIDB_EPI_DICE if kind == "dice" else N.PIDB_EPI_IOU,
+               n, p, p + 8 * n, p + 16 * n, inv, ii, io, d, out.rank.data_ptr(),
+               stream_ptr(dev))
+        return buf, out
+
+    buf, out = _graphed(de, kind, enqueue)
     host = buf[n:].cpu().numpy()
     if float(host[n]) == 0.0:
         raise DegenerateEnsembleError("ensemble mean mask is identically zero")

@@ -502,3 +502,33 @@ def test_config2_eid_exact(pb):
     else:
         close(r.depth, c, 1e-12)
     np.testing.assert_array_equal(r.rank, exact.ranks(c))
+
+
+def test_graph_replay_matches_eager(pb, monkeypatch):
+    """Repeated calls on one DeviceEnsemble are captured into a CUDA graph on
+    the second call and replayed afterwards; the graph reads the live member
+    matrix, so in-place updates are seen."""
+    from paper_2512_15187_b200 import depth as D
+
+    rng = np.random.default_rng(12)
+    U = rng.uniform(size=(37, 3000)).astype(np.float32)
+    B = (rng.uniform(size=(29, 2500)) < 0.4).astype(np.float32)
+    cases = [(torch.from_numpy(U).cuda(), ("pid-mean", "pid", "dice", "iou")),
+             (torch.from_numpy(B).cuda(), ("eid",))]
+    for t, methods in cases:
+        de = pb.DeviceEnsemble.from_tensor(t)
+        for meth in methods:
+            runs = [pb.depth_by_method(de, meth) for _ in range(4)]
+            for r in runs[1:]:
+                assert np.array_equal(r.depth, runs[0].depth)
+                np.testing.assert_array_equal(r.rank, runs[0].rank)
+            assert meth in de._cache["graphs"] or meth in ("dice", "iou")
+        # in-place update of the members: the replayed graph sees it
+        with torch.no_grad():
+            de.values[:, :de.m] = torch.flip(de.values[:, :de.m], dims=[0])
+        for meth in methods:
+            got = pb.depth_by_method(de, meth)
+            monkeypatch.setattr(D, "_GRAPHS", False)
+            want = pb.depth_by_method(de, meth)
+            monkeypatch.setattr(D, "_GRAPHS", True)
+            assert np.array_equal(got.depth, want.depth)
