@@ -25,7 +25,7 @@ constexpr int kMode_MEAN = 0, kMode_COLS = 1, kMode_MASS = 2, kMode_SIM = 3;  //
 constexpr int kColThreads = 256;
 constexpr int kRowThreads = 256;
 constexpr int kRowWarps = kRowThreads / 32;
-constexpr int kRowsPerWarp = 16;
+constexpr int kRowsPerWarp = 16;  // even: rows are swept in pairs
 constexpr int kRowBlock = kRowWarps * kRowsPerWarp;  // 128 members per CTA
 constexpr int kChunkCells = 2048;                    // cells per SMEM stage of f/w
 
@@ -141,17 +141,17 @@ __global__ void __launch_bounds__(kRowThreads)
     }
     __syncthreads();
     const int64_t cells = m - xb < kChunkCells ? m - xb : kChunkCells;
+    // two member rows per pass and eight 16-byte loads in flight per lane
 #pragma unroll 1
-    for (int k = 0; k < kRowsPerWarp; ++k) {
-      const int64_t r = rbase + (int64_t)k * kRowWarps;
-      if (r >= n) break;
-      const T* row = u + r * ld + xb;
-      double ar = 0.0, am = 0.0;
-      int64_t nb = 0;
-#pragma unroll 4
-      for (int i = lane * EPC; i < cells; i += kStep) {
-        double v[EPC];
-        WVec<T>::load(row + i, v);
+    for (int k = 0; k < kRowsPerWarp; k += 2) {
+      const int64_t r0 = rbase + (int64_t)k * kRowWarps;
+      if (r0 >= n) break;
+      const bool two = r0 + kRowWarps < n;
+      const T* row0 = u + r0 * ld + xb;
+      const T* row1 = two ? row0 + (int64_t)kRowWarps * ld : row0;
+      double ar0 = 0.0, am0 = 0.0, ar1 = 0.0, am1 = 0.0;
+      int64_t nb0 = 0, nb1 = 0;
+      auto body = [&](const double (&v)[EPC], int i, double& ar, double& am, int64_t& nb) {
 #pragma unroll
         for (int e = 0; e < EPC; ++e) {
           const bool in = i + e < cells;
@@ -168,10 +168,23 @@ __global__ void __launch_bounds__(kRowThreads)
             am = fma(x, wx, am);
           }
         }
+      };
+#pragma unroll 4
+      for (int i = lane * EPC; i < cells; i += kStep) {
+        double v0[EPC], v1[EPC];
+        WVec<T>::load(row0 + i, v0);
+        WVec<T>::load(row1 + i, v1);
+        body(v0, i, ar0, am0, nb0);
+        if (two) body(v1, i, ar1, am1, nb1);
       }
-      acc_row[k] += ar;
-      acc_mass[k] += am;
-      acc_nb[k] += nb;
+      acc_row[k] += ar0;
+      acc_mass[k] += am0;
+      acc_nb[k] += nb0;
+      if (two) {
+        acc_row[k + 1] += ar1;
+        acc_mass[k + 1] += am1;
+        acc_nb[k + 1] += nb1;
+      }
     }
   }
 #pragma unroll
