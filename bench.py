@@ -524,6 +524,9 @@ def run_eid_secondary(args, dev, pk):
     ms = timed(lambda: pb.depth_eid(de), max(1, min(args.steps, 10)), 3, 1)
     ev = D.KERNEL_EVENTS
     D.KERNEL_EVENTS = None
+    # the same calls without the per-kernel event hooks: repeated calls on one
+    # DeviceEnsemble then replay a captured CUDA graph
+    ms_graph = timed(lambda: pb.depth_eid(de), max(1, min(args.steps, 10)), 3, 1)
     kg, _ = kernel_ms(ev, "pidb_gram_i8")
     km, _ = kernel_ms(ev, "pidb_member_masses")
     cpu = None
@@ -540,7 +543,8 @@ def run_eid_secondary(args, dev, pk):
                              "peak": INT8_TOPS_PROBE, "frac": ops / (kg * 1e-3) / 1e12 / INT8_TOPS_PROBE,
                              "kernel_ms": kg, "algorithmic_ops": ops,
                              "peak_src": "cuBLAS INT8 probe (torch._int_mm 8192^3)"},
-           "masses_ms": km}
+           "masses_ms": km,
+           "ms_per_depth_graph": ms_graph}
     if cpu is not None:
         out["cpu_baseline"] = cpu
     del de
