@@ -89,3 +89,40 @@ def test_no_cpu_fallback():
 def test_unknown_method_rejected_before_any_device_work():
     with pytest.raises(pb.ValidationError):
         pb.depth_pid(np.zeros((2, 3)), algorithm="bogus")
+
+
+def test_ensemble_operations_like_the_reference():
+    """grid.py:159-296 behaviours (reference tests/test_grid.py TestEnsemble,
+    TestPermuteCells; binarize)."""
+    g = pb.GridSpec((4,))
+    masks = [pb.ProbMask(g, u) for u in TRIO]
+    e = pb.Ensemble(g, masks, ids=["c0", "c1", "c2"])
+    np.testing.assert_array_equal(e.block_values(1, 3), TRIO[1:3])
+    assert e.subset([2, 0]).ids == ("c2", "c0")
+    calls = []
+
+    def loader(i):
+        def f():
+            calls.append(i)
+            return masks[i]
+        return f
+
+    lazy = pb.Ensemble(g, [loader(i) for i in range(3)])
+    mapped = lazy.map_members(lambda m: pb.binarize(m, 0.5).to_prob())
+    assert calls == [] and mapped.is_lazy()
+    np.testing.assert_array_equal(mapped.member(1).values, TRIO[1])
+    assert calls == [1]
+    with pytest.raises(pb.GridMismatchError):  # a loader on another grid fails on access
+        pb.Ensemble(g, [lambda: pb.ProbMask(pb.GridSpec((2, 2)), np.zeros(4))]).member(0)
+    perm = np.array([3, 1, 0, 2])
+    p = pb.permute_cells(e, perm)
+    np.testing.assert_array_equal(p.member(0).values, TRIO[0][perm])
+    with pytest.raises(pb.ValidationError):
+        pb.permute_cells(e, np.array([0, 0, 1, 2]))
+    # binarize compares in the member dtype (numpy: Python float -> float32)
+    u = pb.ProbMask(g, np.full(4, np.float32(0.7)))
+    assert pb.binarize(u, 0.7).bits.all()
+    with pytest.raises(pb.ValidationError):
+        pb.binarize(u, 0.0)
+    with pytest.raises(pb.ValidationError):
+        pb.binarize_ensemble(e, 1.5)
