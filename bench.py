@@ -476,7 +476,7 @@ def run_pid_secondary(args, rank, world, pg, dev, pk):
                              "frac": ach / pk["hbm_gbs"], "kernels_ms": [k1, k2],
                              "algorithmic_bytes": 2 * b, "note": "exact fp64, two HBM passes"}
         else:
-            kg, _ = kernel_ms(ev, "pidb_gram_tf32x3")
+            kg, _ = kernel_ms(ev, "pidb_gram_tf32x3_sums")
             flops = n * (n + 1) * de.m  # symmetric Gram, 2 flops per MAC
             ach = flops / (kg * 1e-3) / 1e12
             o["roofline"] = {"bound": "tensor", "achieved": ach, "unit": "TFLOP/s",

@@ -133,6 +133,15 @@ int pidb_gram_tf32x3(const float* u, int64_t n, int64_t m, int64_t ld,
                      const double* w, double* gram, void* ws, size_t ws_bytes,
                      void* stream);
 
+/* K1 with the PID sums fused into its epilogue (no N x N Gram in HBM):
+ *   row_plain[i] = sum_j G[i,j],  col_inv[i] = sum_j inv_j G[i,j]
+ * (depth.py:156-160 with G symmetric), inv = inverse masses (n, device).
+ * Same workspace as pidb_gram_tf32x3; outputs are additive over cell
+ * shards. */
+int pidb_gram_tf32x3_sums(const float* u, int64_t n, int64_t m, int64_t ld,
+                          const double* w, const double* inv, double* row_plain,
+                          double* col_inv, void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- K4 ----
  * Gram -> (row_plain, col_inv): row_plain[i] = sum_j G[i,j],
  * col_inv[j] = sum_i inv[i] G[i,j]  (depth.py:155-160). */

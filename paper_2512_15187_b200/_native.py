@@ -71,6 +71,7 @@ SIGNATURES: dict[str, tuple] = {
     "pidb_validate": (_int, [_p, _int, _i64, _i64, _i64, _int, _p, _p]),
     "pidb_synth_ellipsoids": (_int, [_p, _i64, _i64, _i64, _p, _dbl, _p]),
     "pidb_synth_disks": (_int, [_p, _i64, _i64, _i64, _p, _dbl, _p]),
+    "pidb_gram_tf32x3_sums": (_int, [_p, _i64, _i64, _i64, _p, _p, _p, _p, _p, _sz, _p]),
     "pidb_band_envelopes": (_int, [_p, _int, _i64, _i64, _i64, _p, _i64, _dbl, _p, _int, _p, _p,
                                    _p]),
 }

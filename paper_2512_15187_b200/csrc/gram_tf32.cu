@@ -45,7 +45,10 @@ struct GramTf32Params {
   int64_t m, ld;
   const float* u;
   const double* w;   // nullable
-  double* part;      // [units][kB][kB]
+  double* part;      // [units][kB][kB]   (Gram tiles), or
+  const double* inv; // fused sums: inverse masses (n)
+  double* vpart;     // [units][4][kB]: tile row sums, inv-weighted row sums,
+                     //                 column sums, inv-weighted column sums
 };
 
 __device__ __forceinline__ void tile_of(int t, int& ib, int& jb) {
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // shadow -> global fp64 split partial (row = quad*32 + lane)
     double* dst = p.part + ((size_t)unit * kB + quad * 32 + lane) * kB;
 #pragma unroll 1
-    for (int c = 0; c < kB; c += 16) {
+    for (int c = 0; c < kB && p.vpart == nullptr; c += 16) {
       uint32_t sh[32];
       if (nflush > 0) {
         tc::tmem_ld32(lane_base + 256 + (uint32_t)(2 * c), sh);
@@ -289,9 +292,90 @@ __global__ void __launch_bounds__(kThreads, 1)
                          __hiloint2double((int)sh[2 * e + 3], (int)sh[2 * e + 2]));
     }
   }
+  if (p.vpart != nullptr) {
+    // Fused epilogue (no N x N Gram in HBM): the fp64 tile goes to SMEM (the
+    // operand ring is idle once every role has left its loop; rows padded to
+    // kB + 1 doubles for the column pass), then 4 x kB tile sums are written:
+    // sum_j G_ij, sum_j inv_j G_ij (rows of block ib), sum_i G_ij,
+    // sum_i inv_i G_ij (columns of block jb).  Fixed order: deterministic.
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    constexpr int kLd = kB + 1;
+    double* tile = reinterpret_cast<double*>(ring);
+    if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+      const int quad = warp & 3;
+      const int r = quad * 32 + lane;
+      const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < kB; c += 16) {
+        uint32_t sh[32];
+        tc::tmem_ld32(lane_base + 256 + (uint32_t)(2 * c), sh);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          tile[r * kLd + c + e] = __hiloint2double((int)sh[2 * e + 1], (int)sh[2 * e]);
+      }
+    }
+    __syncthreads();
+    const int tx = threadIdx.x;
+    double* vp = p.vpart + (size_t)unit * 4 * kB;
+    if (tx < kB) {  // row tx of block ib
+      double a = 0.0, b = 0.0;
+      for (int c = 0; c < kB; ++c) {
+        const int j = jb * kB + c;
+        const double g = tile[tx * kLd + c];
+        a += g;
+        b = fma(j < p.n ? p.inv[j] : 0.0, g, b);
+      }
+      vp[tx] = a;
+      vp[kB + tx] = b;
+    } else if (tx < 2 * kB) {  // column c of block jb
+      const int c = tx - kB;
+      double a = 0.0, b = 0.0;
+      for (int r = 0; r < kB; ++r) {
+        const int i = ib * kB + r;
+        const double g = tile[r * kLd + c];
+        a += g;
+        b = fma(i < p.n ? p.inv[i] : 0.0, g, b);
+      }
+      vp[2 * kB + c] = a;
+      vp[3 * kB + c] = b;
+    }
+  }
   tc::fence_before();
   __syncthreads();
   if (warp == kEpiWarp0) tc::tmem_dealloc(tmem, kTmemCols);
+}
+
+// row_plain[r] = sum_j G_rj, col_inv[r] = sum_j inv_j G_rj (G symmetric) from
+// the fused tile sums: tiles (I(r), jb >= I(r)) contribute their row sums,
+// tiles (ib < I(r), I(r)) their column sums; splits and tiles in fixed order.
+__global__ void gram_tf32_sums_kernel(const double* __restrict__ vpart, int n, int splits,
+                                      double* __restrict__ row_plain,
+                                      double* __restrict__ col_inv) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int R = r / kB, o = r - R * kB;
+    const int nb = (n + kB - 1) / kB;
+    double a = 0.0, b = 0.0;
+    for (int jb = 0; jb < nb; ++jb) {
+      const int ib = min(R, jb), jj = max(R, jb);
+      const int tile = jj * (jj + 1) / 2 + ib;
+      const bool as_row = R <= jb;  // r in the tile's row block
+      for (int s = 0; s < splits; ++s) {
+        const double* vp = vpart + ((size_t)tile * splits + s) * 4 * kB;
+        if (as_row) {
+          a += vp[o];
+          b += vp[kB + o];
+        } else {
+          a += vp[2 * kB + o];
+          b += vp[3 * kB + o];
+        }
+      }
+    }
+    row_plain[r] = a;
+    col_inv[r] = b;
+  }
 }
 
 // G[i][j] = G[j][i] = sum over splits (fixed order) of the tile holding (min, max).
@@ -339,6 +423,32 @@ using namespace pidb;
 extern "C" size_t pidb_gram_tf32x3_workspace_bytes(int64_t n, int64_t m) {
   if (n < 1 || m < 1) return 0;
   return plan(n, m).ws;
+}
+
+extern "C" int pidb_gram_tf32x3_sums(const float* u, int64_t n, int64_t m, int64_t ld,
+                                     const double* w, const double* inv, double* row_plain,
+                                     double* col_inv, void* ws, size_t ws_bytes, void* stream) {
+  PIDB_REQUIRE(u && inv && row_plain && col_inv && n >= 1 && m >= 1,
+               "bad arguments to pidb_gram_tf32x3_sums");
+  PIDB_REQUIRE(ld >= m && (ld * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(u) & 15) == 0,
+               "member rows must be 16-byte aligned with ld >= m");
+  PIDB_REQUIRE(n <= (1 << 16), "too many members for the dense Gram");
+  const Plan g = plan(n, m);
+  PIDB_REQUIRE(ws && ws_bytes >= g.ws, "workspace too small: need %zu bytes", g.ws);
+  GramTf32Params p{};
+  p.n = (int)n; p.nb = g.nb; p.ntiles = g.ntiles; p.splits = g.splits; p.kblocks = g.kblocks;
+  p.kb_per = g.kb_per; p.m = m; p.ld = ld; p.u = u; p.w = w;
+  p.inv = inv;
+  p.vpart = reinterpret_cast<double*>(static_cast<char*>(ws) + 256);
+  cudaStream_t st = (cudaStream_t)stream;
+  PIDB_CUDA(cudaFuncSetAttribute(gram_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)g.smem));
+  gram_tf32_kernel<<<g.units, kThreads, g.smem, st>>>(p);
+  PIDB_LAUNCH_CHECK("gram_tf32_kernel (fused sums)");
+  gram_tf32_sums_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p.vpart, (int)n, g.splits,
+                                                                      row_plain, col_inv);
+  PIDB_LAUNCH_CHECK("gram_tf32_sums_kernel");
+  return PIDB_OK;
 }
 
 extern "C" int pidb_gram_tf32x3(const float* u, int64_t n, int64_t m, int64_t ld, const double* w,

@@ -311,17 +311,20 @@ def _pid_factorized(de: DeviceEnsemble, out: _Out) -> torch.Tensor:
 
 
 def _pid_gram(de: DeviceEnsemble, out: _Out) -> np.ndarray:
-    """PID from the dense N x N Gram on tcgen05 tensor cores (K1 3xTF32)."""
-    from .reduction import gram_device
-
+    """PID from the symmetric N x N Gram on tcgen05 tensor cores (K1 3xTF32),
+    with the row sums and inverse-mass-weighted column sums of G
+    (depth.py:156-160) fused into the Gram epilogue: no N x N matrix in HBM."""
+    if de.dtype_code != N.PIDB_F32:
+        raise ValidationError("the tensor-core Gram takes float32 members")
     n, dev = de.n, de.device
     mass = _masses_device(de)
-    g = gram_device(de)  # allreduced fp64 (n, n)
     inv = out.ptrs()[0]
     N.call("pidb_inverse_masses", n, mass.data_ptr(), inv, stream_ptr(dev))
     rc = _f64(2 * n, dev)
-    N.call("pidb_gram_reduce", g.data_ptr(), n, inv, rc.data_ptr(), rc.data_ptr() + 8 * n,
-           stream_ptr(dev))
+    ws = de.workspace(N.load().pidb_gram_tf32x3_workspace_bytes(n, de.m))
+    _launch("pidb_gram_tf32x3_sums", de.ptr(), n, de.m, de.ld, de.wptr(), inv, rc.data_ptr(),
+            rc.data_ptr() + 8 * n, ws.data_ptr(), ws.numel(), stream_ptr(dev))
+    _allreduce(rc, de)
     _, ii, io, d = out.ptrs()
     N.call("pidb_depth_epilogue", N.PIDB_EPI_PID, n, rc.data_ptr(), mass.data_ptr(),
            rc.data_ptr() + 8 * n, inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
