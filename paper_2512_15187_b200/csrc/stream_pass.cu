@@ -943,11 +943,11 @@ size_t rows_tail(int V, int cs) {
 // (tools/prof_k5.py, 256^3 cells): pairs of CTAs win for
 // n <= 512 and 8-CTA clusters for 1536 < n <= 2048; in between the chunked
 // kernel is faster.  PIDB_CLUSTER overrides (tuning).
-int cluster_size_for(int64_t n, bool ws) {
+int cluster_size_for(int64_t n, bool ws, bool exchange) {
   int cs = 0;
   // warp-specialised: <= 256 rows per CTA; non-portable clusters of up to 16
   // measured faster than (n = 2500, 3000) or equal to (n = 4000) the chunked kernel
-  if (ws) cs = n <= 2048 ? (int)((n + 255) / 256) : 16;
+  if (ws || !exchange) cs = n <= 2048 ? (int)((n + 255) / 256) : 16;
   else if (n <= 512) cs = 2;
   else if (n > 1536 && n <= 2048) cs = 8;
   if (const char* e = std::getenv("PIDB_CLUSTER")) {
@@ -972,7 +972,9 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl, int mode = MODE_MEAN) 
   pl.cs = 1;
   pl.rpc = (int)n;
   if (n > 256 && n <= 16 * 256) {
-    const int cs = cluster_size_for(n, ws_eligible(esize, mode) && std::getenv("PIDB_WS") == nullptr);
+    // the masses-only mode has no column exchange: plain row slices per CTA
+    const int cs = cluster_size_for(n, ws_eligible(esize, mode) && std::getenv("PIDB_WS") == nullptr,
+                                    mode != MODE_MASS);
     if (cs >= 2 && cs <= 16) {
       pl.chunked = false;
       pl.cs = cs;
@@ -1198,11 +1200,18 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
 
 }  // namespace
 
+// One size for every entry point sharing the workspace: the largest plan over
+// the modes (the kernel choice, and with it the grid, depends on the mode).
 size_t stream_pass_workspace(int64_t n, int64_t m, int dtype) {
-  Plan pl;
   if (n < 1 || m < 1) return 0;
-  if (!make_plan(n, m, dtype == PIDB_F32 ? 4 : 8, pl)) return wide_workspace(n, m, dtype);
-  return workspace_bytes(pl, n);
+  size_t need = 0;
+  for (int mode : {MODE_MEAN, MODE_COLS, MODE_MASS, MODE_SIM}) {
+    Plan pl;
+    need = std::max(need, make_plan(n, m, dtype == PIDB_F32 ? 4 : 8, pl, mode)
+                              ? workspace_bytes(pl, n)
+                              : wide_workspace(n, m, dtype));
+  }
+  return need;
 }
 
 }  // namespace pidb

@@ -532,3 +532,16 @@ def test_graph_replay_matches_eager(pb, monkeypatch):
             want = pb.depth_by_method(de, meth)
             monkeypatch.setattr(D, "_GRAPHS", True)
             assert np.array_equal(got.depth, want.depth)
+
+
+@pytest.mark.parametrize("n", [300, 1000, 3000])
+def test_masses_across_kernel_variants(pb, n):
+    """member_masses takes a different kernel than the depth passes (no column
+    exchange); the shared workspace must fit every variant."""
+    U, w = make_fuzzy(4000 + n, n, (37, 29), True)
+    e = ens(pb, U, w, dims=(37, 29))
+    de = pb.stage(e)
+    pb.depth_pid_mean(de)
+    close(pb.member_masses(de), port.masses(U, w), 1e-9)
+    pb.depth_pid(de)
+    close(pb.member_masses(de), port.masses(U, w), 1e-9)
