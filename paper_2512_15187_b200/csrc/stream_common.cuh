@@ -33,6 +33,7 @@ struct StreamParams {
   int mode;
   const double* w;       // nullable
   const double* inv;     // MODE_COLS
+  const double* fvec;    // ext row sweep: per-cell f (w*S, w*T or the mean), else null
   double* part;          // [grid][pncb * n][2]
   double* part_col;      // [grid]
   int64_t* part_nb;      // [grid][n] (MODE_MASS, nullable)
@@ -49,6 +50,7 @@ constexpr int kChunkMax = 16;  // n <= 4096
 
 struct Plan {
   bool chunked;
+  bool ext;     // wide ensembles: row sweep against a precomputed f, row slices per CTA
   int cs, rpc;  // cs > 1: cluster rows kernel
   int rows, stages, grid, box_rows;
   uint32_t stage_bytes;
@@ -283,12 +285,16 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = (int)p.n;
   const bool weighted = p.w != nullptr;
-  const int cs = CL ? p.cs : 1;
-  const uint32_t rank = CL ? cluster_rank() : 0u;
+  // ext (wide ensembles, not CL): f is given, CTA b of a group of p.cs takes
+  // member rows [b * rpc, (b + 1) * rpc) of its tiles; no column sweep
+  const bool ext = !CL && p.fvec != nullptr;
+  const bool sliced = CL || ext;
+  const int cs = sliced ? p.cs : 1;
+  const uint32_t rank = CL ? cluster_rank() : (ext ? blockIdx.x % (unsigned)cs : 0u);
   const int cid = (int)blockIdx.x / cs, ncl = (int)gridDim.x / cs;
-  const int r0 = CL ? (int)rank * p.rpc : 0;
-  const int box = CL ? p.rpc : n;                        // member rows per TMA box
-  const int nloc = CL ? max(0, min(n - r0, p.rpc)) : n;  // member rows of this CTA
+  const int r0 = sliced ? (int)rank * p.rpc : 0;
+  const int box = sliced ? p.rpc : n;                        // member rows per TMA box
+  const int nloc = sliced ? max(0, min(n - r0, p.rpc)) : n;  // member rows of this CTA
   const int64_t my_tiles = p.tiles > cid ? (p.tiles - 1 - cid) / ncl + 1 : 0;
   const uint64_t pol = policy_evict_first();
   const uint32_t xbytes = (uint32_t)cs * V * 8u;
@@ -333,19 +339,26 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         const int64_t x = x0 + tid;
         wx = x < p.m ? (weighted ? __ldg(p.w + x) : 1.0) : 0.0;
       }
-      mbar_wait(&full[s], par);
-      csw.reset();
-      csw.run(tiles + (size_t)s * p.stage_bytes + p1_off, ph, box, SWEEP, p.inv, r0 + ph, n);
-      csw.combine(SWEEP);
-      if (lane < 16) {
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) red[warp * V + q * EPC + e] = csw.part[e];
-      }
-      named_sync(kBarCols, kWsColThreads);
       double S = 0.0;
-      if (tid < V) {
+      if (ext) {
+        if (tid < V) {
+          const int64_t x = x0 + tid;
+          S = x < p.m ? __ldg(p.fvec + x) : 0.0;
+        }
+      } else {
+        mbar_wait(&full[s], par);
+        csw.reset();
+        csw.run(tiles + (size_t)s * p.stage_bytes + p1_off, ph, box, SWEEP, p.inv, r0 + ph, n);
+        csw.combine(SWEEP);
+        if (lane < 16) {
 #pragma unroll
-        for (int k = 0; k < kWsColWarps; ++k) S += red[k * V + tid];
+          for (int e = 0; e < EPC; ++e) red[warp * V + q * EPC + e] = csw.part[e];
+        }
+        named_sync(kBarCols, kWsColThreads);
+        if (tid < V) {
+#pragma unroll
+          for (int k = 0; k < kWsColWarps; ++k) S += red[k * V + tid];
+        }
       }
       // the row group has read sS/sW[b] (and, CL, xbuf slot of tile j-2)
       named_sync(kBarSFree + b, kAll);
@@ -360,6 +373,14 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           for (int c = 0; c < cs; ++c) st_async_f64x2(mapa(la, c), S, S1, mapa(lb, c));
         }
         if (tid < V) sW[b * V + tid] = wx;
+      } else if (ext) {
+        // S holds f: w*S (MEAN), w*T (COLS) or the mean S/n (SIM); the column
+        // total sum_x w S is taken once per tile (row block 0)
+        if (tid < V) {
+          sW[b * V + tid] = wx;
+          sS[b * V + tid] = S;
+          if (rank == 0) col_acc += MODE == MODE_SIM ? wx * S * (double)p.n : S;
+        }
       } else {
         if (tid < V) {
           sW[b * V + tid] = wx;
@@ -378,9 +399,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     named_arrive(kBarSFree + 0, kAll);  // both S buffers start free
     named_arrive(kBarSFree + 1, kAll);
     int s = 0;
+    uint32_t rpar = 0;
     for (int64_t j = 0; j < my_tiles; ++j) {
       const int b = (int)(j & 1);
       named_sync(kBarSReady + b, kAll);
+      if (ext) mbar_wait(&full[s], rpar);  // no column sweep has waited on the stage
       double s_l[EPL], w_l[EPL];
       if constexpr (CL) {
         const int slot = (int)(j & 3);
@@ -443,7 +466,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         // every row thread passed its xbar wait for tile j: re-arm for tile j+4
         if (CL && j + 4 < my_tiles) mbar_arrive_expect_tx(&xbar[j & 3], xbytes);
       }
-      if (++s == p.stages) s = 0;
+      if (++s == p.stages) { s = 0; rpar ^= 1u; }
     }
 #pragma unroll
     for (int k = 0; k < ROWS; ++k) {
@@ -510,7 +533,7 @@ int launch_cluster(K kern, const CUtensorMap& tm, StreamParams& sp, const Plan& 
 template <typename T>
 int launch_ws(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStream_t st) {
   const int rw = kRowsWarps - ws_col_warps(sp.mode);
-  if (pl.cs > 1) {
+  if (pl.cs > 1 && !pl.ext) {
     const int rows = (pl.rpc + rw - 1) / rw;
     switch (sp.mode * 64 + rows) {
 #define PIDB_WSC_CASE(M, R) \
@@ -531,8 +554,8 @@ int launch_ws(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStrea
       default: return kNotHandled;
     }
   }
-  sp.groups = pl.grid;
-  const int rows = (int)((sp.n + rw - 1) / rw);
+  if (!pl.ext) sp.groups = pl.grid;  // ext: the caller sets the slice groups
+  const int rows = (int)(((pl.ext ? pl.rpc : sp.n) + rw - 1) / rw);
   switch (sp.mode * 32 + rows) {
 #define PIDB_WS_CASE(M, R) \
   case M * 32 + R: return launch(rows_ws_kernel<T, R, M, false>, tm, sp, pl, st);

@@ -38,6 +38,9 @@ namespace pidb {
 
 // stream_wide.cu: two-read fallback for n > 4096 members
 size_t wide_workspace(int64_t n, int64_t m, int dtype);
+size_t wide_fold_bytes(int64_t n, int64_t m, int dtype);
+int wide_fold_f(int mode, const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                const double* w, const double* inv, void* ws, const double** f, void* stream);
 int run_wide_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
                   const double* w, const double* inv, double* out_row, double* out_mass,
                   double* out_col, int64_t* out_nb, void* ws, size_t ws_bytes, void* stream);
@@ -533,6 +536,7 @@ size_t chunked_smem(int V) {
 bool ws_eligible(int mode) { return mode != MODE_MASS; }
 
 bool make_plan(int64_t n, int64_t m, int esize, Plan& pl, int mode = MODE_MEAN) {
+  pl = Plan{};
   if (n < 1 || m < 1) return false;
   const int V = kRowBytes / esize;
   pl.tiles = (m + V - 1) / V;
@@ -633,6 +637,86 @@ int launch_typed(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaSt
   return PIDB_EUNSUPPORTED;
 }
 
+// Wide ensembles (n > 4096): one column sweep (stream_wide.cu) gives f, then
+// the warp-specialised row sweep reads member-row slices of <= 256 rows per
+// CTA: nrb slices per tile and ncl tile streams, nrb * ncl <= #SMs (one wave).
+struct ExtPlan {
+  int nrb, box, ncl, grid, stages;
+  uint32_t stage_bytes;
+  size_t smem, fold, parts;
+};
+
+ExtPlan ext_plan(int64_t n, int64_t m, int esize) {
+  ExtPlan e{};
+  const int sms = sm_count();
+  const int min_nrb = (int)((n + 255) / 256);
+  e.ncl = std::max(1, sms / std::max(1, min_nrb));
+  e.nrb = std::max(min_nrb, sms / e.ncl);
+  e.box = (int)((n + e.nrb - 1) / e.nrb);
+  e.nrb = (int)((n + e.box - 1) / e.box);
+  e.grid = e.nrb * e.ncl;
+  const int V = kRowBytes / esize;
+  e.stage_bytes = (uint32_t)align_up((size_t)e.box * kRowBytes, 1024);
+  const size_t tb = rows_tail(V, 1) + 1024;
+  e.stages = (int)std::min<size_t>(kMaxStages, (kSmemBudget - tb) / e.stage_bytes);
+  e.smem = (size_t)e.stages * e.stage_bytes + tb;
+  e.fold = align_up(wide_fold_bytes(n, m, esize == 4 ? PIDB_F32 : PIDB_F64), 256);
+  e.parts = align_up((size_t)e.ncl * n * 2 * sizeof(double), 256) +
+            align_up((size_t)e.grid * sizeof(double), 256) +
+            align_up((size_t)e.ncl * n * sizeof(int64_t), 256);
+  return e;
+}
+
+size_t ext_workspace(int64_t n, int64_t m, int dtype) {
+  const ExtPlan e = ext_plan(n, m, dtype == PIDB_F32 ? 4 : 8);
+  return e.fold + e.parts;
+}
+
+int run_ext_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                 const double* w, const double* inv, double* out_row, double* out_mass,
+                 double* out_col, void* ws, size_t ws_bytes, void* stream) {
+  const int es = dtype == PIDB_F32 ? 4 : 8;
+  const ExtPlan e = ext_plan(n, m, es);
+  if (ws == nullptr || ws_bytes < e.fold + e.parts) {
+    set_error("workspace too small: need %zu bytes, got %zu", e.fold + e.parts, ws_bytes);
+    return PIDB_EWORKSPACE;
+  }
+  const double* f = nullptr;
+  int rc = wide_fold_f(mode, u, dtype, n, m, ld, w, inv, ws, &f, stream);
+  if (rc != PIDB_OK) return rc;
+  CUtensorMap tm;
+  rc = encode_tma_2d(&tm, u,
+                     dtype == PIDB_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                     (uint64_t)m, (uint64_t)n, (uint64_t)ld * es, (uint32_t)(kRowBytes / es),
+                     (uint32_t)e.box, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (rc != PIDB_OK) return rc;
+  char* base = static_cast<char*>(ws) + e.fold;
+  StreamParams sp{};
+  sp.counter = reinterpret_cast<unsigned*>(ws);  // offset 0: zero between launches
+  sp.n = n; sp.m = m; sp.tiles = (m + kRowBytes / es - 1) / (kRowBytes / es);
+  sp.stages = e.stages; sp.stage_bytes = e.stage_bytes; sp.mode = mode;
+  sp.cs = e.nrb; sp.rpc = e.box; sp.groups = e.ncl;
+  sp.w = w; sp.inv = inv; sp.fvec = f;
+  sp.part = reinterpret_cast<double*>(base);
+  base += align_up((size_t)e.ncl * n * 2 * sizeof(double), 256);
+  sp.part_col = reinterpret_cast<double*>(base);
+  base += align_up((size_t)e.grid * sizeof(double), 256);
+  sp.part_nb = nullptr;
+  sp.out_row = out_row; sp.out_mass = out_mass; sp.out_col = out_col; sp.out_nb = nullptr;
+  Plan pl{};
+  pl.chunked = false; pl.ext = true; pl.cs = e.nrb; pl.rpc = e.box; pl.grid = e.grid;
+  pl.stages = e.stages; pl.stage_bytes = e.stage_bytes; pl.smem = e.smem; pl.box_rows = e.box;
+  pl.tiles = sp.tiles;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  rc = dtype == PIDB_F32 ? launch_ws_f32(tm, sp, pl, st) : launch_ws_f64(tm, sp, pl, st);
+  if (rc == kNotHandled) {
+    set_error("no warp-specialised kernel for %d rows per CTA", e.box);
+    return PIDB_EUNSUPPORTED;
+  }
+  return rc;
+}
+
 int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
                     const double* w, const double* inv, double* out_row, double* out_mass,
                     double* out_col, int64_t* out_nb, void* ws, size_t ws_bytes, void* stream) {
@@ -644,10 +728,14 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
   PIDB_REQUIRE(ld >= m && (ld * es) % 16 == 0,
                "row stride %lld must be >= m and a multiple of 16 bytes", (long long)ld);
   PIDB_REQUIRE((reinterpret_cast<uintptr_t>(u) & 15) == 0, "member matrix must be 16-byte aligned");
-  Plan pl;
-  if (!make_plan(n, m, es, pl, mode))
+  Plan pl{};
+  if (!make_plan(n, m, es, pl, mode)) {
+    if (mode != MODE_MASS && std::getenv("PIDB_WS") == nullptr)
+      return run_ext_pass(mode, u, dtype, n, m, ld, w, inv, out_row, out_mass, out_col, ws,
+                          ws_bytes, stream);
     return run_wide_pass(mode, u, dtype, n, m, ld, w, inv, out_row, out_mass, out_col, out_nb, ws,
                          ws_bytes, stream);
+  }
   const size_t need = workspace_bytes(pl, n);
   if (ws == nullptr || ws_bytes < need) {
     set_error("workspace too small: need %zu bytes, got %zu", need, ws_bytes);
@@ -687,10 +775,10 @@ size_t stream_pass_workspace(int64_t n, int64_t m, int dtype) {
   if (n < 1 || m < 1) return 0;
   size_t need = 0;
   for (int mode : {MODE_MEAN, MODE_COLS, MODE_MASS, MODE_SIM}) {
-    Plan pl;
+    Plan pl{};
     need = std::max(need, make_plan(n, m, dtype == PIDB_F32 ? 4 : 8, pl, mode)
                               ? workspace_bytes(pl, n)
-                              : wide_workspace(n, m, dtype));
+                              : std::max(wide_workspace(n, m, dtype), ext_workspace(n, m, dtype)));
   }
   return need;
 }

@@ -264,6 +264,39 @@ size_t wide_workspace(int64_t n, int64_t m, int dtype) {
   return b;
 }
 
+// Column sweep only (C(x) over all members, folded to f = w*C, or C/n for the
+// similarity mode) for the warp-specialised row sweep of wide ensembles.  f
+// is left at workspace offset 256 (m doubles); returns the bytes used.
+size_t wide_fold_bytes(int64_t n, int64_t m, int dtype) {
+  const WidePlan pl = wide_plan(n, m, dtype == PIDB_F32 ? 4 : 8);
+  return 256 + align_up((size_t)pl.col_groups * pl.mpad * sizeof(double), 256) +
+         align_up((size_t)pl.fold_blocks * sizeof(double), 256);
+}
+
+int wide_fold_f(int mode, const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                const double* w, const double* inv, void* ws, const double** f, void* stream) {
+  const WidePlan pl = wide_plan(n, m, dtype == PIDB_F32 ? 4 : 8);
+  char* base = static_cast<char*>(ws) + 256;
+  double* part = reinterpret_cast<double*>(base);
+  double* colpart =
+      reinterpret_cast<double*>(base + align_up((size_t)pl.col_groups * pl.mpad * sizeof(double), 256));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const dim3 cg((unsigned)pl.col_xblocks, (unsigned)pl.col_groups);
+  const double* coef = mode == kMode_COLS ? inv : nullptr;
+  if (dtype == PIDB_F32)
+    wide_col_kernel<float><<<cg, kColThreads, 0, st>>>(static_cast<const float*>(u), n, m, ld, coef,
+                                                       pl.rows_per_group, part, pl.mpad);
+  else
+    wide_col_kernel<double><<<cg, kColThreads, 0, st>>>(static_cast<const double*>(u), n, m, ld,
+                                                        coef, pl.rows_per_group, part, pl.mpad);
+  PIDB_LAUNCH_CHECK("wide_col_kernel");
+  wide_fold_kernel<<<pl.fold_blocks, 256, 0, st>>>(part, pl.col_groups, pl.mpad, m, n, w, mode,
+                                                   colpart);
+  PIDB_LAUNCH_CHECK("wide_fold_kernel");
+  *f = part;
+  return PIDB_OK;
+}
+
 int run_wide_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
                   const double* w, const double* inv, double* out_row, double* out_mass,
                   double* out_col, int64_t* out_nb, void* ws, size_t ws_bytes, void* stream) {
