@@ -513,6 +513,7 @@ int launch_cluster(K kern, const CUtensorMap& tm, StreamParams& sp, const Plan& 
   cfg.gridDim = dim3((unsigned)(pl.grid / pl.cs * pl.cs));
   int active = 0;
   PIDB_CUDA(cudaOccupancyMaxActiveClusters(&active, kern, &cfg));
+  if (std::getenv("PIDB_TEST_NO_CLUSTER")) active = 0;  // test hook: exercise the fallback
   if (active < 1) {
     set_error("no co-resident cluster of %d CTAs for the streaming kernel", pl.cs);
     return PIDB_EUNSUPPORTED;

@@ -535,6 +535,8 @@ size_t chunked_smem(int V) {
 
 bool ws_eligible(int mode) { return mode != MODE_MASS; }
 
+thread_local bool t_no_cluster = false;  // set while falling back from a cluster launch
+
 bool make_plan(int64_t n, int64_t m, int esize, Plan& pl, int mode = MODE_MEAN) {
   pl = Plan{};
   if (n < 1 || m < 1) return false;
@@ -543,7 +545,7 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl, int mode = MODE_MEAN) 
   pl.grid = (int)std::min<int64_t>(pl.tiles, sm_count());
   pl.cs = 1;
   pl.rpc = (int)n;
-  if (n > 256 && n <= 16 * 256) {
+  if (n > 256 && n <= 16 * 256 && !t_no_cluster) {
     // the masses-only mode has no column exchange: plain row slices per CTA
     // (fp64 masses measured faster with the chunked kernel: 6.3 vs 5.3 TB/s)
     const int cs = cluster_size_for(n, ws_eligible(mode) && std::getenv("PIDB_WS") == nullptr,
@@ -588,11 +590,14 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl, int mode = MODE_MEAN) 
   return true;
 }
 
+// Sized for a full-width grid whatever the plan, so that a launch can fall
+// back to another kernel variant without a bigger workspace.
 size_t workspace_bytes(const Plan& pl, int64_t n) {
+  const size_t g = (size_t)std::max(pl.grid, sm_count());
   size_t b = 256;  // completion counter: fixed offset 0, zero between launches
-  b += align_up((size_t)pl.grid * 2 * n * 2 * sizeof(double), 256);
-  b += align_up((size_t)pl.grid * sizeof(double), 256);
-  b += align_up((size_t)pl.grid * n * sizeof(int64_t), 256);
+  b += align_up(g * 2 * n * 2 * sizeof(double), 256);
+  b += align_up(g * sizeof(double), 256);
+  b += align_up(g * n * sizeof(int64_t), 256);
   return b;
 }
 
@@ -763,8 +768,17 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
   sp.part_nb = out_nb ? reinterpret_cast<int64_t*>(base) : nullptr;
   sp.out_row = out_row; sp.out_mass = out_mass; sp.out_col = out_col; sp.out_nb = out_nb;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return dtype == PIDB_F32 ? launch_typed<float>(tm, sp, pl, st)
-                           : launch_typed<double>(tm, sp, pl, st);
+  rc = dtype == PIDB_F32 ? launch_typed<float>(tm, sp, pl, st)
+                         : launch_typed<double>(tm, sp, pl, st);
+  if (rc == PIDB_EUNSUPPORTED && pl.cs > 1 && !t_no_cluster) {
+    // no co-resident cluster of this size right now (shared or partitioned
+    // GPU): the same pass with the cluster-free kernels
+    t_no_cluster = true;
+    rc = run_stream_pass(mode, u, dtype, n, m, ld, w, inv, out_row, out_mass, out_col, out_nb, ws,
+                         ws_bytes, stream);
+    t_no_cluster = false;
+  }
+  return rc;
 }
 
 }  // namespace

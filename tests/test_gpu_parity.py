@@ -545,3 +545,15 @@ def test_masses_across_kernel_variants(pb, n):
     close(pb.member_masses(de), port.masses(U, w), 1e-9)
     pb.depth_pid(de)
     close(pb.member_masses(de), port.masses(U, w), 1e-9)
+
+
+def test_cluster_fallback(pb, monkeypatch):
+    """Without a co-resident cluster (shared / partitioned GPU) the pass runs
+    on the cluster-free kernels with the same results."""
+    U, w = make_fuzzy(77, 700, (31, 33), True)
+    e = ens(pb, U, w, dims=(31, 33))
+    want = pb.depth_pid(e)
+    monkeypatch.setenv("PIDB_TEST_NO_CLUSTER", "1")
+    got = pb.depth_pid(e)
+    close(got.depth, want.depth, 1e-13)
+    np.testing.assert_array_equal(got.rank, want.rank)
