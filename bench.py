@@ -431,6 +431,8 @@ def run_e2e(args, host, _, meta, fn, world, pg, dev):
     total = n * int(np.prod(dims))
     return {"value": total / (ms * 1e-3), "unit": "member-voxels/s", "ms_per_step": ms,
             "h2d_bytes_per_step": n * m * 4, "d2h_bytes_per_step": n * 8 * 4 + n * 8 + 24,
+            "h2d_GBps_effective": n * m * 4 / (ms * 1e-3) / 1e9,
+            "bound": "PCIe host-to-device copy (the kernels take ~1.5% of the step)",
             "path": "depth_pid_mean(DeviceEnsemble.from_tensor(pinned host tensor)): "
                     "pitched H2D + device validation + K5 + K4 + result D2H"}
 
