@@ -430,7 +430,7 @@ def run_e2e(args, host, _, meta, fn, world, pg, dev):
     ms = timed(step, max(1, min(args.steps, 3)), 1, world)
     total = n * int(np.prod(dims))
     return {"value": total / (ms * 1e-3), "unit": "member-voxels/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": n * m * 4, "d2h_bytes_per_step": n * 8 * 4 + n * 8 + 24,
+            "h2d_bytes_per_step": n * m * 4, "d2h_bytes_per_step": (5 * n + n + 1) * 8,
             "h2d_GBps_effective": n * m * 4 / (ms * 1e-3) / 1e9,
             "bound": "PCIe host-to-device copy (the kernels take ~1.5% of the step)",
             "path": "depth_pid_mean(DeviceEnsemble.from_tensor(pinned host tensor)): "
