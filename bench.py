@@ -150,8 +150,23 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
-def timed(step, steps, warmup, world, sampler=None):
-    """W untimed steps, then K steps between barrier+sync, device events."""
+_L2_FLUSH = None
+
+
+def flush_l2():
+    """Write 512 MB (> the 126 MB L2) so the next step starts cold."""
+    import torch
+
+    global _L2_FLUSH
+    if _L2_FLUSH is None:
+        _L2_FLUSH = torch.empty(128 << 20, dtype=torch.float32, device="cuda")
+    _L2_FLUSH.fill_(1.0)
+
+
+def timed(step, steps, warmup, world, sampler=None, flush=False):
+    """W untimed steps, then K steps between barrier+sync, device events.
+    flush=True (inputs smaller than L2): each step is timed on its own with
+    an L2 flush between steps, outside the timed intervals."""
     import torch
 
     for _ in range(warmup):
@@ -159,20 +174,33 @@ def timed(step, steps, warmup, world, sampler=None):
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
     if sampler:
         sampler.__enter__()
         time.sleep(0.3)
-    a.record()
-    for _ in range(steps):
-        step()
-    b.record()
-    torch.cuda.synchronize()
+    if flush:
+        total = 0.0
+        for _ in range(steps):
+            flush_l2()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            step()
+            b.record()
+            b.synchronize()
+            total += a.elapsed_time(b)
+        ms = total / steps
+    else:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            step()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
     if sampler:
         sampler.__exit__()
     barrier(world)
-    ms = a.elapsed_time(b) / steps
     return max_over_ranks(ms, world)
 
 
@@ -202,6 +230,21 @@ def ellipsoid_sample_cpu(res, n, y_planes, seed=0):
         d = r * (1.0 - 1.0 / rho)
         u = torch.where(rho > 1.0, torch.exp(-(d ** 2) / (2.0 * sigma * sigma)), torch.ones_like(rho))
         out[i] = u.to(torch.float32).reshape(-1).numpy()
+    return out
+
+
+def disk_sample_cpu(res, n, seed=0):
+    """cfg1 members on the host (gen_disk_ensemble recipe, numpy)."""
+    from paper_2512_15187_b200.synth import disk_params
+
+    prm, sigma2, _ = disk_params(res, n, seed)
+    y, x = np.mgrid[0:res, 0:res].astype(np.float64)
+    out = np.empty((n, res * res), dtype=np.float32)
+    for i in range(n):
+        cy, cx, radius = prm[i]
+        dist = np.sqrt((y - cy) ** 2 + (x - cx) ** 2)
+        out[i] = np.where(dist <= radius, 1.0,
+                          np.exp(-((dist - radius) ** 2) / (2.0 * sigma2))).reshape(-1)
     return out
 
 
@@ -242,11 +285,10 @@ def run_reference(args, rank, world):
     method, res, n, desc = WORKLOADS[args.workload]
     workers = os.cpu_count() or 1
     planes = args.ref_planes or (8 if res >= 512 else max(1, res // 16))
-    U = ellipsoid_sample_cpu(res, n, planes) if args.workload != "cfg1" else None
-    if U is None:
-        from paper_2512_15187_b200.synth import disk_params
-
-        raise SystemExit("reference arm supports ellipsoid workloads")
+    if args.workload == "cfg1":  # the whole 2D ensemble (26 MB)
+        U, planes = disk_sample_cpu(res, n), res
+    else:
+        U = ellipsoid_sample_cpu(res, n, planes)
     if method == "pid":
         U = U[: min(n, args.ref_pid_members)]
     mv = U.shape[0] * U.shape[1]
@@ -303,12 +345,18 @@ def run_ours(args, rank, world, local, pg):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     method, res, n, desc = WORKLOADS[args.workload]
-    m_full = res ** 3
+    two_d = args.workload == "cfg1"
+    m_full = res ** 2 if two_d else res ** 3
     shard = (rank, world) if world > 1 else None
     fn = pb.depth_pid_mean if method == "pid-mean" else pb.depth_pid
     pk = peaks()
 
-    de = synth.ellipsoids_device(res, n, 0, 0, device=dev, shard=shard, process_group=pg)
+    if two_d:  # reference gen_disk_ensemble recipe (SURVEY.md §8 d: no 2D ellipse generator)
+        if shard is not None:
+            raise SystemExit("cfg1 (26 MB) is a single-GPU workload")
+        de = synth.disks_device(res, n, 0, device=dev)
+    else:
+        de = synth.ellipsoids_device(res, n, 0, 0, device=dev, shard=shard, process_group=pg)
     torch.cuda.synchronize()
     m_local = de.m
 
@@ -319,7 +367,8 @@ def run_ours(args, rank, world, local, pg):
     sampler = ClockSampler(local) if rank == 0 else None
     fn(de)  # first call outside the event log (plans, workspace)
     D.KERNEL_EVENTS = []
-    ms = timed(step, args.steps, args.warmup, world, sampler)
+    small = n * m_local * 4 < 2 * 126e6  # inputs not much larger than L2: flush between steps
+    ms = timed(step, args.steps, args.warmup, world, sampler, flush=small)
     kname = "pidb_pid_mean_partials"
     kms, klaunch = kernel_ms(D.KERNEL_EVENTS, kname)
     launches_per_step = 3 if method == "pid-mean" else 6
@@ -337,8 +386,9 @@ def run_ours(args, rank, world, local, pg):
         "data": "synthetic (reference gen_ellipsoid_ensemble recipe: per-member Philox "
                 "parameters on the host, voxels evaluated on the device)",
         "config": {"workload": desc, "members": n, "cells": m_full, "cells_per_gpu": m_local,
-                   "bytes_per_gpu": alg_bytes, "l2": "no flush: inputs (%.1f GB/GPU) >> 126 MB L2"
-                   % (alg_bytes / 1e9),
+                   "bytes_per_gpu": alg_bytes, "l2": ("L2 flushed (512 MB write) between individually timed steps: inputs "
+                          "(%.3f GB) < 2 x 126 MB L2" if small else
+                          "no flush: inputs (%.1f GB/GPU) >> 126 MB L2") % (alg_bytes / 1e9),
                    "parallelism": f"voxel-sharded x{world}, one NCCL allreduce of 2N+1 fp64"
                    if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "kernel": "stream_pass_kernel (K5, pidb_pid_mean_partials)",
@@ -364,6 +414,8 @@ def run_ours(args, rank, world, local, pg):
         planes = args.ref_planes or (8 if res >= 512 else max(1, res // 16))
         y0 = res // 2 - planes // 2
         lo, hi = y0 * res * res, (y0 + planes) * res * res
+        if two_d:  # all of cfg1
+            lo, hi, planes = 0, res * res, res
         U = de.values[:, lo:hi].cpu().numpy()
         if method == "pid":
             U = U[: args.ref_pid_members]
