@@ -588,7 +588,7 @@ def run_eid_secondary(args, dev, pk):
         U = de.values[:100, : res * res].cpu().numpy()
         cpu = cpu_pair_baseline(U, "eid", n, res * res, "cfg2 (full 512^2 grid)")
     m = res * res
-    ops = 2.0 * n * n * m
+    ops = float(n) * (n + 1) * m  # symmetric Gram (upper triangle), 2 ops per MAC
     out = {"workload": "cfg2: eID, 500 binary contours 512^2 (bit-exact integer path)",
            "ms_per_depth": ms, "value": n * m / (ms * 1e-3), "unit": "member-voxels/s",
            "pair_voxels_per_s": n * n * m / (ms * 1e-3),
