@@ -1,0 +1,77 @@
+"""Randomised parity sweep of every streaming-kernel variant against the CPU
+oracle: python tools/fuzz_parity.py SECONDS [seed]
+(n log-uniform in 1..6000, cells log-uniform, fp32/fp64, weighted or not,
+PID-mean / PID / dice / IoU / masses, and binary eID; depths within 1e-11,
+ranks equal wherever the oracle's depth gaps exceed 1e-11)."""
+import sys
+import time
+import warnings
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2512_15187_b200 as pb  # noqa: E402
+from oracle import exact, port  # noqa: E402
+
+warnings.simplefilter("ignore", RuntimeWarning)  # the CV warning of skewed random draws
+budget = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+t_end = time.time() + budget
+cases = fails = 0
+
+
+def ranks_ok(got, want_depth, want_rank):
+    if np.array_equal(got, want_rank):
+        return True
+    d = np.sort(want_depth)
+    return np.min(np.diff(d)) < 1e-11 if d.size > 1 else False
+
+
+while time.time() < t_end:
+    n = int(np.exp(rng.uniform(0, np.log(6000))))
+    m = int(np.exp(rng.uniform(0, np.log(min(200000, 4e7 / n)))))
+    f64 = rng.uniform() < 0.25
+    weighted = rng.uniform() < 0.4
+    binary = rng.uniform() < 0.2
+    U = rng.uniform(size=(n, m))
+    if binary:
+        U = (U < rng.uniform(0.2, 0.8)).astype(np.float64)
+    U = U.astype(np.float64 if f64 else np.float32)
+    w = rng.uniform(0.5, 2.0, size=m) if weighted else None
+    de = pb.DeviceEnsemble.from_tensor(torch.from_numpy(U), w)
+    checks = []
+    try:
+        if U.sum() > 0:
+            r, ref = pb.depth_pid_mean(de), port.depth_pid_mean(U, w, workers=8)
+            checks.append(("pid-mean", r, ref))
+            for meas in ("dice", "iou"):
+                checks.append((meas, pb.depth_similarity_baseline(de, meas),
+                               port.depth_similarity(U, meas, w, workers=8)))
+        if n * n * m <= 4e10:
+            checks.append(("pid", pb.depth_pid(de), port.depth_pid(U, w, workers=8)))
+        mass = pb.member_masses(de)
+        ok = np.allclose(mass, port.masses(U, w), rtol=1e-12, atol=1e-9)
+        if not ok:
+            print(f"FAIL masses n={n} m={m} f64={f64} w={weighted}", flush=True)
+            fails += 1
+        if binary and not weighted and n * n * m <= 4e10:
+            a, b, c, _ = exact.eid_fast(U.astype(np.float32))
+            r = pb.depth_eid(de)
+            if not (np.array_equal(r.depth, c) and np.array_equal(r.rank, exact.ranks(c))):
+                print(f"FAIL eid n={n} m={m}", flush=True)
+                fails += 1
+        for name, r, ref in checks:
+            err = float(np.max(np.abs(r.depth - ref["depth"]))) if n else 0.0
+            if err > 1e-11 or not ranks_ok(r.rank, ref["depth"], ref["rank"]):
+                print(f"FAIL {name} n={n} m={m} f64={f64} w={weighted} bin={binary} err={err:.2e}",
+                      flush=True)
+                fails += 1
+    except Exception as exc:  # report and continue
+        print(f"ERROR n={n} m={m} f64={f64} w={weighted}: {type(exc).__name__}: {exc}", flush=True)
+        fails += 1
+    cases += 1
+    del de
+print(f"fuzz_parity: {cases} cases, {fails} failures", flush=True)
+sys.exit(1 if fails else 0)
