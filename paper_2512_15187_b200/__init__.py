@@ -46,6 +46,8 @@ from .grid import (
 )
 from .inclusion import fuzzy_dice, prob_inclusion, prob_iou, subset_epsilon
 from .reduction import gram_block
+from .synth import (gen_contour_ensemble_2d, gen_disk_ensemble, gen_ellipsoid_ensemble,
+                    gen_fuzzy_disk)
 from .fuzzify import ScalarField, default_width, fuzzy_isocontour, hard_isocontour, normalize_density
 from .boxplot import Band, BoxplotArtifact, build_boxplot, emit_slice_images, write_pgm
 from .consistency import RankScatter, kendall_tau, pearson, rank_scatter, stability_test
@@ -107,6 +109,10 @@ __all__ = [
     "depth_pid_mean",
     "depth_similarity_baseline",
     "fuzzy_dice",
+    "gen_contour_ensemble_2d",
+    "gen_disk_ensemble",
+    "gen_ellipsoid_ensemble",
+    "gen_fuzzy_disk",
     "gram_block",
     "mask_mass",
     "mass_cv",

@@ -159,6 +159,20 @@ class DeviceEnsemble:
         return cls.from_tensor(torch.from_numpy(arr), grid.weights, ids,
                                tuple(grid.dims), validate=False, device=device)
 
+    # reference Ensemble duck-typing (grid.py:194-212): host copies of members
+    def member(self, i: int):
+        from .grid import ProbMask
+
+        if self.sharded:
+            raise ValidationError("a sharded ensemble holds only this rank's cells")
+        return ProbMask(self.grid, self.values[i, :self.m].cpu().numpy())
+
+    def __iter__(self):
+        return (self.member(i) for i in range(self.n))
+
+    def block_values(self, lo: int, hi: int) -> np.ndarray:
+        return self.values[lo:hi, :self.m].cpu().numpy()
+
     def subset(self, indices: Sequence[int]) -> "DeviceEnsemble":
         """Members ``indices`` in the given order (grid.py Ensemble.subset);
         one device-side row gather, same grid and weights."""

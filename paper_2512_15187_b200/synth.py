@@ -15,6 +15,8 @@ import torch
 
 from . import _native as N
 from .device import DeviceEnsemble, padded_ld, require_cuda, shard_bounds, stream_ptr
+from .errors import ValidationError
+from .grid import GridSpec, ProbMask
 
 
 def member_rng(seed: int, index: int) -> np.random.Generator:
@@ -134,4 +136,51 @@ def disks_device(res, n, seed=0, device=None) -> DeviceEnsemble:
 def contours_device(n, res, seed=0, device=None) -> DeviceEnsemble:
     masks = contour_masks(n, res, seed)
     return DeviceEnsemble.from_tensor(torch.from_numpy(masks), ids=[f"contour_{i:04d}" for i in range(n)],
+                                      dims=(res, res), validate=False, device=device)
+
+
+# ------------------------------------------------- the reference's names
+
+
+def gen_fuzzy_disk(grid2d: GridSpec, center, radius: float, sigma2: float) -> ProbMask:
+    """One fuzzy disk mask (synth.py:30-51): 1 inside, Gaussian falloff
+    exp(-(dist - radius)^2 / (2 sigma2)) outside (host, float64 -> float32)."""
+    if len(grid2d.dims) != 2:
+        raise ValidationError("gen_fuzzy_disk needs a 2D grid")
+    if not radius > 0.0 or not sigma2 > 0.0:
+        raise ValidationError("radius and sigma2 must be positive")
+    yy, xx = np.meshgrid(*(np.arange(d, dtype=np.float64) for d in grid2d.dims), indexing="ij")
+    dist = np.sqrt((yy - center[0]) ** 2 + (xx - center[1]) ** 2)
+    u = np.where(dist <= radius, 1.0, np.exp(-((dist - radius) ** 2) / (2.0 * sigma2)))
+    return ProbMask(grid2d, u.astype(np.float32))
+
+
+def gen_disk_ensemble(res: int, n: int, seed: int, device=None, **kw) -> DeviceEnsemble:
+    """gen_disk_ensemble (synth.py:54-81), generated in HBM."""
+    if res < 8 or n < 1:
+        raise ValidationError("need res >= 8 and n >= 1")
+    if kw:
+        raise ValidationError(f"unsupported generator options {sorted(kw)}")
+    return disks_device(res, n, seed, device=device)
+
+
+def gen_ellipsoid_ensemble(res: int, n_base: int, n_outliers: int, seed: int, device=None,
+                           **kw) -> DeviceEnsemble:
+    """gen_ellipsoid_ensemble (synth.py:84-135), generated in HBM."""
+    if res < 8:
+        raise ValidationError("need res >= 8")
+    if n_base < 0 or n_outliers < 0 or n_base + n_outliers < 1:
+        raise ValidationError("need n_base, n_outliers >= 0 and at least one member")
+    if kw:
+        raise ValidationError(f"unsupported generator options {sorted(kw)}")
+    return ellipsoids_device(res, n_base, n_outliers, seed, device=device)
+
+
+def gen_contour_ensemble_2d(n: int, res: int, seed: int, device=None, **kw) -> DeviceEnsemble:
+    """gen_contour_ensemble_2d (synth.py:165-210): binary Fourier contours."""
+    if n < 1 or res < 8:
+        raise ValidationError("need n >= 1 and res >= 8")
+    masks = contour_masks(n, res, seed, **kw)
+    return DeviceEnsemble.from_tensor(torch.from_numpy(masks),
+                                      ids=[f"contour_{i:04d}" for i in range(n)],
                                       dims=(res, res), validate=False, device=device)

@@ -241,6 +241,19 @@ def test_device_synth_matches_reference_generators(pb):
     np.testing.assert_allclose(de.values[:, :de.m].cpu().numpy(), z["U"], rtol=2e-7, atol=1e-30)
     z = golden("gen_contours")
     np.testing.assert_array_equal(synth.contour_masks(10, 32, 0), z["U"])
+    # the reference-named wrappers (synth.py:54-210), DeviceEnsembles that
+    # also duck-type as reference Ensembles
+    e = pb.gen_disk_ensemble(64, 12, 0)
+    assert e.ids[0] == "disk_0000" and e.dims == (64, 64)
+    np.testing.assert_allclose(e.block_values(0, 12), golden("gen_disks")["U"], rtol=2e-7, atol=1e-30)
+    e = pb.gen_ellipsoid_ensemble(16, 8, 2, 0)
+    assert e.ids[-1] == "outlier_0001" and len(list(e)) == 10
+    np.testing.assert_allclose(e.member(3).values, golden("gen_ellipsoids")["U"][3], rtol=2e-7,
+                               atol=1e-30)
+    e = pb.gen_contour_ensemble_2d(10, 32, 0)
+    np.testing.assert_array_equal(e.block_values(0, 10), golden("gen_contours")["U"])
+    with pytest.raises(pb.ValidationError):
+        pb.gen_disk_ensemble(4, 3, 0)
 
 
 # ---------------------------------------------------- reference hand values

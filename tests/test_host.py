@@ -126,3 +126,19 @@ def test_ensemble_operations_like_the_reference():
         pb.binarize(u, 0.0)
     with pytest.raises(pb.ValidationError):
         pb.binarize_ensemble(e, 1.5)
+
+
+def test_gen_fuzzy_disk_matches_reference_members():
+    """gen_fuzzy_disk (synth.py:30-51) on the host: the reference's disk
+    members (golden gen_disks = gen_disk_ensemble(64, 12, 0)) bit for bit."""
+    from conftest import golden
+    from paper_2512_15187_b200.synth import disk_params
+
+    z = golden("gen_disks")
+    prm, sigma2, _ = disk_params(64, 12, 0)
+    g = pb.GridSpec((64, 64))
+    for i in (0, 5, 11):
+        cy, cx, r = prm[i]
+        assert np.array_equal(pb.gen_fuzzy_disk(g, (cy, cx), r, sigma2).values, z["U"][i])
+    with pytest.raises(pb.ValidationError):
+        pb.gen_fuzzy_disk(pb.GridSpec((4,)), (0, 0), 1.0, 1.0)
