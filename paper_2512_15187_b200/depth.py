@@ -182,10 +182,11 @@ def _masses_device(de: DeviceEnsemble, with_nonbinary: bool = False):
     return (mass, nb) if with_nonbinary else mass
 
 
-def _mean_partials(de: DeviceEnsemble) -> torch.Tensor:
+def _mean_partials(de: DeviceEnsemble, buf: torch.Tensor | None = None) -> torch.Tensor:
     """K5: packed [row_plain (n) | mass (n) | col_mean (1)], allreduced."""
     dev = de.device
-    buf = _f64(2 * de.n + 1, dev)
+    if buf is None:
+        buf = _f64(2 * de.n + 1, dev)
     wsb = N.load().pidb_pid_mean_workspace_bytes(de.n, de.m, de.dtype_code)
     if wsb == 0:
         raise ValidationError(f"ensemble of {de.n} members is not supported by the tile layout")
@@ -211,20 +212,32 @@ def _col_sums(de: DeviceEnsemble, inv: torch.Tensor) -> torch.Tensor:
 class _Out:
     """Device result block [inv | in_in | in_out | depth] + ranks, one D2H."""
 
-    def __init__(self, n: int, dev):
+    def __init__(self, n: int, dev, extra: int = 0):
         self.n = n
-        self.block = _f64(5 * n, dev)  # one allocation -> one D2H
+        # one allocation -> one D2H; `extra` fp64 slots after the results carry
+        # the method's partial sums (masses, mean mass) in the same copy
+        self.block = _f64(5 * n + extra, dev)
         self.vals = self.block[:4 * n]
-        self.rank = self.block[4 * n:].view(torch.int64)
+        self.rank = self.block[4 * n:5 * n].view(torch.int64)
+        self.extra = self.block[5 * n:]
+        self._host = None
 
     def ptrs(self):
         p, n = self.vals.data_ptr(), self.n
         return p, p + 8 * n, p + 16 * n, p + 24 * n
 
+    def host(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self.block.cpu().numpy()
+        return self._host
+
+    def host_extra(self) -> np.ndarray:
+        return self.host()[5 * self.n:]
+
     def fetch(self):
-        h = self.block.cpu().numpy()
-        v = h[:4 * self.n].reshape(4, self.n)
-        r = h[4 * self.n:].view(np.int64)
+        h, n = self.host(), self.n
+        v = h[:4 * n].reshape(4, n)
+        r = h[4 * n:5 * n].view(np.int64)
         return v[1].copy(), v[2].copy(), v[3].copy(), r.copy()
 
 
@@ -270,16 +283,17 @@ def depth_pid_mean(ensemble, workers: int | None = None,
     n, dev = de.n, de.device
 
     def enqueue():
-        buf = _mean_partials(de)
-        out = _Out(n, dev)
+        out = _Out(n, dev, extra=2 * n + 1)
+        buf = _mean_partials(de, out.extra)
         p = buf.data_ptr()
         inv, ii, io, d = out.ptrs()
         N.call("pidb_depth_epilogue", N.PIDB_EPI_PID_MEAN, n, p, p + 8 * n, p + 16 * n,
                inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
         return buf, out
 
-    buf, out = _graphed(de, "pid-mean", enqueue)
-    host = buf[n:].cpu().numpy()
+    _, out = _graphed(de, "pid-mean", enqueue)
+    out._host = None
+    host = out.host_extra()[n:]
     masses, col_mean = host[:n], float(host[n])
     if col_mean == 0.0:
         raise DegenerateEnsembleError("ensemble mean mask is identically zero")
@@ -299,7 +313,7 @@ def _pid_factorized(de: DeviceEnsemble, out: _Out) -> torch.Tensor:
     inverse-mass-weighted column sums (SURVEY.md §0 finding 2).  Queues the
     work and returns the K5 block [row_plain | mass | col]."""
     n, dev = de.n, de.device
-    buf = _mean_partials(de)
+    buf = _mean_partials(de, out.extra if out.extra.numel() >= 2 * n + 1 else None)
     p = buf.data_ptr()
     inv = out.ptrs()[0]
     N.call("pidb_inverse_masses", n, p + 8 * n, inv, stream_ptr(dev))
@@ -357,11 +371,12 @@ def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") 
         masses = _pid_gram(de, out)
     else:
         def enqueue():
-            out = _Out(n, de.device)
+            out = _Out(n, de.device, extra=2 * n + 1)
             return _pid_factorized(de, out), out
 
-        buf, out = _graphed(de, "pid", enqueue)
-        masses = buf[n:2 * n].cpu().numpy()
+        _, out = _graphed(de, "pid", enqueue)
+        out._host = None
+        masses = out.host_extra()[n:2 * n].copy()
     return _finish(de, out, "pid", masses, t0)
 
 
@@ -393,10 +408,11 @@ def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
             return nb, out
 
         nb, out = _graphed(de, "eid", enqueue)
+        out._host = None  # a replayed graph reuses the same result block
         # one host round trip: the non-binary check is read after the whole
         # stream has been queued (the results are discarded if it fails)
         _raise_first_nonbinary(de, nb)
-        masses = out.vals[:n].cpu().numpy()
+        masses = out.host()[:n].copy()
     else:
         out = _Out(n, dev)
         mass, nb = _masses_device(de, with_nonbinary=True)
@@ -434,21 +450,22 @@ def depth_similarity_baseline(ensemble, measure: str, workers: int | None = None
     n, dev = de.n, de.device
 
     def enqueue():
-        buf = _f64(2 * n + 1, dev)
+        out = _Out(n, dev, extra=2 * n + 1)
+        buf = out.extra
         ws = de.workspace(N.load().pidb_pid_mean_workspace_bytes(de.n, de.m, de.dtype_code))
         p = buf.data_ptr()
         _launch("pidb_similarity_partials", de.ptr(), de.dtype_code, n, de.m, de.ld, de.wptr(),
                 p, p + 8 * n, p + 16 * n, ws.data_ptr(), ws.numel(), stream_ptr(dev))
         _allreduce(buf, de)
-        out = _Out(n, dev)
         inv, ii, io, d = out.ptrs()
         N.call("pidb_depth_epilogue", N.PIDB_EPI_DICE if kind == "dice" else N.PIDB_EPI_IOU,
                n, p, p + 8 * n, p + 16 * n, inv, ii, io, d, out.rank.data_ptr(),
                stream_ptr(dev))
         return buf, out
 
-    buf, out = _graphed(de, kind, enqueue)
-    host = buf[n:].cpu().numpy()
+    _, out = _graphed(de, kind, enqueue)
+    out._host = None
+    host = out.host_extra()[n:]
     if float(host[n]) == 0.0:
         raise DegenerateEnsembleError("ensemble mean mask is identically zero")
     return _finish(de, out, kind, host[:n], t0)
