@@ -147,6 +147,13 @@ struct ColSweep {
   }
 };
 
+// Row partials are stored member-major, part[r][cb][g] (g = partial group),
+// so that the reduction below reads each member's groups with coalesced loads.
+__device__ __forceinline__ size_t part_at(const StreamParams& p, int pncb, int cb, int64_t r,
+                                          int g) {
+  return ((size_t)r * pncb + cb) * p.groups + g;
+}
+
 // CTA column partial -> global; the last CTA to finish reduces every CTA's
 // partials in a fixed order (grid, then half) and resets the counter.
 template <int NT>
@@ -172,29 +179,69 @@ __device__ __forceinline__ void finish_partials(const StreamParams& p, int pncb,
   if (*s_ticket != (unsigned)(G - 1)) return;
 
   __threadfence();
-  for (int r = warp; r < n; r += (NT / 32)) {
-    double a = 0.0, b = 0.0;
-    int64_t nb = 0;
-    for (int g = lane; g < p.groups; g += 32) {
-      for (int cb = 0; cb < pncb; ++cb) {
-        const double* src = p.part + ((size_t)g * pncb * n + cb * n + r) * 2;
-        a += __ldcg(src);
-        b += __ldcg(src + 1);
-      }
-      if (p.mode == MODE_MASS && p.part_nb != nullptr)
-        nb += (int64_t)__ldcg(reinterpret_cast<const long long*>(p.part_nb + (size_t)g * n + r));
-    }
-    a = warp_sum(a);
-    b = warp_sum(b);
+  // Every partial load of a round is issued before the first add (kFR rows
+  // x kFG groups per lane): this tail runs on one SM; group-major partials
+  // read one 16-byte word per line cost ~75 us at n = 200.
+  constexpr int kFR = 1, kFG = 5;
+  const bool want_nb = p.mode == MODE_MASS && p.part_nb != nullptr;
+  for (int r0 = warp * kFR; r0 < n; r0 += (NT / 32) * kFR) {
+    double a[kFR], b[kFR];
+    int64_t nb[kFR];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
-    if (lane == 0) {
-      if (p.mode == MODE_MASS) {
-        p.out_mass[r] = b;
-        if (p.out_nb) p.out_nb[r] = nb;
-      } else {
-        p.out_row[r] = a;
-        if (p.out_mass) p.out_mass[r] = b;
+    for (int j = 0; j < kFR; ++j) { a[j] = 0.0; b[j] = 0.0; nb[j] = 0; }
+    for (int g0 = 0; g0 < p.groups; g0 += 32 * kFG) {
+      for (int cb = 0; cb < pncb; ++cb) {
+        double2 v[kFR][kFG];
+#pragma unroll
+        for (int j = 0; j < kFR; ++j)
+#pragma unroll
+          for (int q = 0; q < kFG; ++q) {
+            const int g = g0 + q * 32 + lane, r = r0 + j;
+            v[j][q] = make_double2(0.0, 0.0);
+            if (g < p.groups && r < n)
+              v[j][q] = __ldcg(reinterpret_cast<const double2*>(p.part + part_at(p, pncb, cb, r, g) * 2));
+          }
+#pragma unroll
+        for (int j = 0; j < kFR; ++j)
+#pragma unroll
+          for (int q = 0; q < kFG; ++q) {
+            a[j] += v[j][q].x;
+            b[j] += v[j][q].y;
+          }
+      }
+      if (want_nb) {
+        long long v[kFR][kFG];
+#pragma unroll
+        for (int j = 0; j < kFR; ++j)
+#pragma unroll
+          for (int q = 0; q < kFG; ++q) {
+            const int g = g0 + q * 32 + lane, r = r0 + j;
+            v[j][q] = (g < p.groups && r < n)
+                          ? __ldcg(reinterpret_cast<const long long*>(p.part_nb + part_at(p, 1, 0, r, g)))
+                          : 0ll;
+          }
+#pragma unroll
+        for (int j = 0; j < kFR; ++j)
+#pragma unroll
+          for (int q = 0; q < kFG; ++q) nb[j] += (int64_t)v[j][q];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kFR; ++j) {
+      const int r = r0 + j;
+      const double aj = warp_sum(a[j]);
+      const double bj = warp_sum(b[j]);
+      int64_t nj = nb[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nj += __shfl_xor_sync(0xffffffffu, nj, o);
+      if (lane == 0 && r < n) {
+        if (p.mode == MODE_MASS) {
+          p.out_mass[r] = bj;
+          if (p.out_nb) p.out_nb[r] = nj;
+        } else {
+          p.out_row[r] = aj;
+          if (p.out_mass) p.out_mass[r] = bj;
+        }
       }
     }
   }
@@ -474,7 +521,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       const double a = warp_sum(acc_row[k]);
       const double c = warp_sum(acc_mass[k]);
       if (lane == 0 && rl < nloc) {
-        double* dst = p.part + ((size_t)cid * n + r0 + rl) * 2;
+        double* dst = p.part + part_at(p, 1, 0, r0 + rl, cid) * 2;
         dst[0] = a;
         dst[1] = c;
       }

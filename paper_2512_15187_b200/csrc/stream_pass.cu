@@ -250,10 +250,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
     if (lane == 0 && rl < nloc) {
       const int r = r0 + rl;
-      double* dst = p.part + ((size_t)cid * n + r) * 2;
+      double* dst = p.part + part_at(p, 1, 0, r, cid) * 2;
       dst[0] = a;
       dst[1] = b;
-      if (p.mode == MODE_MASS && p.part_nb != nullptr) p.part_nb[(size_t)cid * n + r] = nb;
+      if (p.mode == MODE_MASS && p.part_nb != nullptr) p.part_nb[part_at(p, 1, 0, r, cid)] = nb;
     }
   }
   if constexpr (CL) cluster_sync();  // no CTA leaves while peers may still target its SMEM
@@ -471,23 +471,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
-  // halves -> global partials (part layout [grid][2 * n][2])
+  // halves -> global partials (member-major: part[r][half][block][2])
 #pragma unroll
   for (int c = 0; c < CMAX; ++c) {
     const int r = c * kChunkRows + b_rr;
     if (c < C && r < n) {
-      double* dst = p.part + ((size_t)blockIdx.x * 2 * n + b_half * n + r) * 2;
+      double* dst = p.part + part_at(p, 2, b_half, r, blockIdx.x) * 2;
       dst[0] = acc_row[c];
       dst[1] = acc_mass[c];
     }
   }
   if (p.mode == MODE_MASS && p.part_nb != nullptr) {
-    int64_t* nbp = p.part_nb + (size_t)blockIdx.x * n;
+    int64_t* nbp = p.part_nb;
     if (b_half == 0) {
 #pragma unroll
       for (int c = 0; c < CMAX; ++c) {
         const int r = c * kChunkRows + b_rr;
-        if (c < C && r < n) nbp[r] = acc_nb[c];
+        if (c < C && r < n) nbp[part_at(p, 1, 0, r, blockIdx.x)] = acc_nb[c];
       }
     }
     __syncthreads();
@@ -496,7 +496,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < CMAX; ++c) {
         const int r = c * kChunkRows + b_rr;
         if (c < C && r < n)
-          atomicAdd(reinterpret_cast<unsigned long long*>(&nbp[r]), (unsigned long long)acc_nb[c]);
+          atomicAdd(reinterpret_cast<unsigned long long*>(&nbp[part_at(p, 1, 0, r, blockIdx.x)]),
+                    (unsigned long long)acc_nb[c]);
       }
     }
   }
