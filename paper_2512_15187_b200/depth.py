@@ -20,6 +20,7 @@ invariance, reduction.py:115-127).
 from __future__ import annotations
 
 import os
+import threading
 import time
 import warnings
 from dataclasses import dataclass
@@ -122,6 +123,10 @@ def _launch(name: str, *args) -> None:
 
 # CUDA graphs for repeated calls on one DeviceEnsemble (PIDB_GRAPHS=0: off)
 _GRAPHS = os.environ.get("PIDB_GRAPHS", "1") != "0"
+# Callers may come from any thread (the reference's contract): captures are
+# serialised and run in thread-local capture mode, so other threads keep
+# launching (and allocating) while one thread records a graph.
+_GRAPH_LOCK = threading.RLock()
 
 
 def _graphed(de: DeviceEnsemble, key: str, enqueue):
@@ -135,16 +140,18 @@ def _graphed(de: DeviceEnsemble, key: str, enqueue):
     (KERNEL_EVENTS) stay eager."""
     if not _GRAPHS or de.sharded or KERNEL_EVENTS is not None:
         return enqueue()
-    cache = de._cache.setdefault("graphs", {})
-    ent = cache.get(key)
+    with _GRAPH_LOCK:
+        cache = de._cache.setdefault("graphs", {})
+        ent = cache.get(key)
+        if ent is None:
+            cache[key] = False
+        elif ent is False:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                outs = enqueue()
+            ent = cache[key] = (g, outs)
     if ent is None:
-        cache[key] = False
         return enqueue()
-    if ent is False:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            outs = enqueue()
-        ent = cache[key] = (g, outs)
     g, outs = ent
     g.replay()
     return outs

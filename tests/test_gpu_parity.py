@@ -547,6 +547,34 @@ def test_graph_replay_matches_eager(pb, monkeypatch):
             assert np.array_equal(got.depth, want.depth)
 
 
+def test_concurrent_callers(pb):
+    """The reference's entry points are callable from any thread
+    (SURVEY.md §8b): threads sharing one DeviceEnsemble (graph capture and
+    replay included) and threads on their own ensembles all get the
+    single-threaded results."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(21)
+    shared = pb.DeviceEnsemble.from_tensor(
+        torch.from_numpy(rng.uniform(size=(40, 5000)).astype(np.float32)).cuda())
+    own = [pb.DeviceEnsemble.from_tensor(
+        torch.from_numpy(rng.uniform(size=(20 + 7 * k, 3000)).astype(np.float32)).cuda())
+        for k in range(4)]
+    methods = ("pid-mean", "pid", "dice")
+    want = {(id(d), m): pb.depth_by_method(d, m).depth for d in [shared, *own] for m in methods}
+
+    def work(k):
+        bad = 0
+        for it in range(12):
+            d = shared if (it + k) % 2 == 0 else own[k]
+            m = methods[(it + k) % len(methods)]
+            bad += not np.array_equal(pb.depth_by_method(d, m).depth, want[(id(d), m)])
+        return bad
+
+    with ThreadPoolExecutor(4) as pool:
+        assert sum(pool.map(work, range(4))) == 0
+
+
 @pytest.mark.parametrize("n", [300, 1000, 3000])
 def test_masses_across_kernel_variants(pb, n):
     """member_masses takes a different kernel than the depth passes (no column
