@@ -169,7 +169,9 @@ GramPlan plan_i8(int64_t n, int64_t m) {
   for (int jb = 0; jb < g.njb; ++jb) g.ntiles += std::min(g.nib, 2 * jb + 2);
   g.kblocks = (int)((m + kBK - 1) / kBK);
   const int sms = sm_count();
-  g.splits = std::max(1, std::min(g.kblocks, (sms + g.ntiles - 1) / g.ntiles));
+  // one wave: ceil(sms / ntiles) splits would leave a few CTAs (150 of them
+  // at n = 500) for a second wave that doubles the kernel time
+  g.splits = std::max(1, std::min(g.kblocks, sms / g.ntiles));
   g.kb_per = (g.kblocks + g.splits - 1) / g.splits;
   g.splits = (g.kblocks + g.kb_per - 1) / g.kb_per;
   g.units = g.ntiles * g.splits;
