@@ -139,19 +139,34 @@ __device__ __forceinline__ uint64_t eid_term_bits53(int64_t m_i, int64_t inter) 
   return (uint64_t)__dmul_rn(t, 9007199254740992.0);  // * 2^53, exact
 }
 
+// Warp per member i.  I is symmetric (the reduction mirrors it), so both
+// sums read row i: row += term(m_i, I_ij), col += term(m_j, I_ij), with the
+// masses m_j = I_jj staged per block in shared memory (one strided read per
+// block instead of one per warp).
+constexpr int kDiagChunk = 1024;
 __global__ void eid_exact_kernel(const int64_t* __restrict__ g, int64_t n,
                                  double* __restrict__ in_in, double* __restrict__ in_out,
                                  double* __restrict__ depth, double* __restrict__ mass) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
-  for (int64_t i = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5); i < n;
-       i += warps) {
-    const int64_t mi = g[i * n + i];
+  __shared__ int64_t sdiag[kDiagChunk];
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  for (int64_t base = (int64_t)blockIdx.x * wpb; base < n; base += (int64_t)gridDim.x * wpb) {
+    const int64_t i = base + (threadIdx.x >> 5);
+    const bool live = i < n;
+    const int64_t mi = live ? g[i * n + i] : 0;
     unsigned __int128 row = 0, col = 0;
-    for (int64_t j = lane; j < n; j += 32) {
-      const int64_t mj = g[j * n + j];
-      row += eid_term_bits53(mi, g[i * n + j]);
-      col += eid_term_bits53(mj, g[j * n + i]);
+    for (int64_t j0 = 0; j0 < n; j0 += kDiagChunk) {
+      const int cnt = (int)(n - j0 < kDiagChunk ? n - j0 : kDiagChunk);
+      __syncthreads();
+      for (int t = threadIdx.x; t < cnt; t += blockDim.x) sdiag[t] = g[(j0 + t) * (n + 1)];
+      __syncthreads();
+      if (live) {
+        const int64_t* gi = g + i * n + j0;
+        for (int t = lane; t < cnt; t += 32) {
+          const int64_t gij = gi[t];
+          row += eid_term_bits53(mi, gij);
+          col += eid_term_bits53(sdiag[t], gij);
+        }
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -162,7 +177,7 @@ __global__ void eid_exact_kernel(const int64_t* __restrict__ g, int64_t n,
       row += ((unsigned __int128)rh << 64) | rl;
       col += ((unsigned __int128)ch << 64) | cl;
     }
-    if (lane == 0) {
+    if (live && lane == 0) {
       if (mass) mass[i] = (double)mi;  // |C_i|, exact
       const double rs = __dmul_rn(u128_to_double_rn(row), 1.1102230246251565e-16);  // 2^-53
       const double cs = __dmul_rn(u128_to_double_rn(col), 1.1102230246251565e-16);
