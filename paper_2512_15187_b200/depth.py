@@ -234,9 +234,19 @@ class _Out:
         return p, p + 8 * n, p + 16 * n, p + 24 * n
 
     def host(self) -> np.ndarray:
-        if self._host is None:
-            self._host = self.block.cpu().numpy()
-        return self._host
+        h = self._host
+        if h is None:
+            h = self._host = self.block.cpu().numpy()
+        return h
+
+    def fresh(self) -> "_Out":
+        """Per-call view of a replayed graph's result block with its own
+        host copy (the block itself is shared by every replay, and callers
+        may come from several threads)."""
+        o = object.__new__(_Out)
+        o.__dict__.update(self.__dict__)
+        o._host = None
+        return o
 
     def host_extra(self) -> np.ndarray:
         return self.host()[5 * self.n:]
@@ -299,7 +309,7 @@ def depth_pid_mean(ensemble, workers: int | None = None,
         return buf, out
 
     _, out = _graphed(de, "pid-mean", enqueue)
-    out._host = None
+    out = out.fresh()
     host = out.host_extra()[n:]
     masses, col_mean = host[:n], float(host[n])
     if col_mean == 0.0:
@@ -382,7 +392,7 @@ def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") 
             return _pid_factorized(de, out), out
 
         _, out = _graphed(de, "pid", enqueue)
-        out._host = None
+        out = out.fresh()
         masses = out.host_extra()[n:2 * n].copy()
     return _finish(de, out, "pid", masses, t0)
 
@@ -415,7 +425,7 @@ def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
             return nb, out
 
         nb, out = _graphed(de, "eid", enqueue)
-        out._host = None  # a replayed graph reuses the same result block
+        out = out.fresh()  # a replayed graph reuses the same result block
         # one host round trip: the non-binary check is read after the whole
         # stream has been queued (the results are discarded if it fails)
         _raise_first_nonbinary(de, nb)
@@ -471,7 +481,7 @@ def depth_similarity_baseline(ensemble, measure: str, workers: int | None = None
         return buf, out
 
     _, out = _graphed(de, kind, enqueue)
-    out._host = None
+    out = out.fresh()
     host = out.host_extra()[n:]
     if float(host[n]) == 0.0:
         raise DegenerateEnsembleError("ensemble mean mask is identically zero")
