@@ -149,6 +149,9 @@ def _graphed(de: DeviceEnsemble, key: str, enqueue):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, capture_error_mode="thread_local"):
                 outs = enqueue()
+            for ws in de._cache.pop("graph_ws_pending", []):
+                ws.zero_()  # the kernels leave their counters at zero after each replay
+                de._cache.setdefault("graph_ws", []).append(ws)
             ent = cache[key] = (g, outs)
     if ent is None:
         return enqueue()

@@ -14,6 +14,7 @@ member on each rank (multi-GPU voxel sharding).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -188,6 +189,14 @@ class DeviceEnsemble:
     def workspace(self, nbytes: int) -> torch.Tensor:
         """Zero-initialised per-device workspace (the kernels leave their
         completion counters at zero on exit, so it is reused as is)."""
+        if torch.cuda.is_current_stream_capturing():
+            # a graph gets its own workspace (alive as long as this ensemble's
+            # graphs): capture streams come from a pool, so a stream-keyed
+            # one could end up shared by graphs replayed on different streams.
+            # Zeroed once after the capture (depth._graphed), not per replay.
+            ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=self.device)
+            self._cache.setdefault("graph_ws_pending", []).append(ws)
+            return ws
         key = ("ws", self.device, torch.cuda.current_stream(self.device).cuda_stream)
         ws = _WS.get(key)
         if ws is None or ws.numel() < nbytes:
