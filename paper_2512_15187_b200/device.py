@@ -14,7 +14,6 @@ member on each rank (multi-GPU voxel sharding).
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass, field
 from typing import Sequence
 
