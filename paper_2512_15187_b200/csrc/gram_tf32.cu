@@ -18,6 +18,10 @@
 // second kernel.  Warps (672 threads): 0 MMA issuer, 1-4 epilogue (one TMEM
 // lane quadrant each), 5-20 converters (LDG.128 operand loads, two stages
 // in flight in registers, hi/lo split written to the swizzled stages).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
 #include "tcgen05.cuh"
 
 namespace pidb {
@@ -47,9 +51,68 @@ struct GramTf32Params {
   const double* w;   // nullable
   double* part;      // [units][kB][kB]   (Gram tiles), or
   const double* inv; // fused sums: inverse masses (n)
-  double* vpart;     // [units][4][kB]: tile row sums, inv-weighted row sums,
-                     //                 column sums, inv-weighted column sums
+  double* vpart;     // [pieces][max_seg][4][kB]: tile row sums, inv-weighted row
+                     //   sums, column sums, inv-weighted column sums
+  // fused sums only: stream-K partition of the whole (tile, k-block) work
+  int pieces, max_seg, w_off, w_diag;
+  int64_t total;
 };
+
+// Stream-K partition (fused-sums path).  The work is a line of units, K-range
+// round q (`splits` rounds of `kb_per` k-blocks) major and tile t (triangular
+// order) minor -- so CTAs running at the same time read the same K window of
+// the operand panels, as the plain split-K launch does -- unit (q, t) costing
+// len(q) * (w_diag for a diagonal tile that shares its operand, else w_off).
+// The line is cut into `pieces` (one per SM) equal parts; a piece covers the
+// tail of one unit, whole units and the head of another, one segment each,
+// every segment writing its own partial slot.
+__host__ __device__ __forceinline__ int64_t sk_col_of(int64_t t) {  // column block of tile t
+  int64_t jb = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while (jb * (jb + 1) / 2 > t) --jb;
+  while ((jb + 1) * (jb + 2) / 2 <= t) ++jb;
+  return jb;
+}
+__host__ __device__ __forceinline__ int64_t sk_len(const GramTf32Params& p, int q) {
+  const int64_t k0 = (int64_t)q * p.kb_per, k1 = k0 + p.kb_per;
+  return (k1 < p.kblocks ? k1 : p.kblocks) - k0;
+}
+// start cost of unit u (u may equal splits * ntiles); diagonal tiles before t = its column block
+__host__ __device__ __forceinline__ int64_t sk_u0(const GramTf32Params& p, int64_t u) {
+  const int64_t q = u / p.ntiles, t = u - q * p.ntiles;
+  const int64_t dw = p.w_off - p.w_diag;
+  const int64_t round = (int64_t)p.w_off * p.ntiles - dw * p.nb;
+  if (q >= p.splits)  // end of the line
+    return (int64_t)p.kb_per * (p.splits - 1) * round + sk_len(p, p.splits - 1) * round;
+  return (int64_t)p.kb_per * q * round + sk_len(p, (int)q) * ((int64_t)p.w_off * t - dw * sk_col_of(t));
+}
+__host__ __device__ __forceinline__ int64_t sk_c(const GramTf32Params& p, int64_t b) {
+  return p.total * b / p.pieces;  // total * pieces < 2^63 (checked by the plan)
+}
+// largest unit u with u0(u) <= c
+__host__ __device__ __forceinline__ int sk_unit_at(const GramTf32Params& p, int64_t c) {
+  int lo = 0, hi = p.splits * p.ntiles - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sk_u0(p, mid) <= c) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+// largest piece b with c(b) <= c
+__host__ __device__ __forceinline__ int sk_piece_at(const GramTf32Params& p, int64_t c) {
+  int lo = 0, hi = p.pieces - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sk_c(p, mid) <= c) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+// k-block offset inside unit u at cost c (consecutive pieces share it: exact partition)
+__host__ __device__ __forceinline__ int64_t sk_kb(int64_t c, int64_t u0, int wt, int64_t len) {
+  const int64_t x = c - u0;
+  if (x <= 0) return 0;
+  const int64_t kb = (x + wt - 1) / wt;
+  return kb < len ? kb : len;
+}
 
 __device__ __forceinline__ void tile_of(int t, int& ib, int& jb) {
   jb = 0;
@@ -82,17 +145,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int unit = blockIdx.x;
-  const int t = unit / p.splits, split = unit - t * p.splits;
-  int ib, jb;
-  tile_of(t, ib, jb);
-  const bool diag = ib == jb;
+  const bool fused = p.vpart != nullptr;
   const bool weighted = p.w != nullptr;
-  const bool share_b = diag && !weighted;  // B operand == A operand
-  const int kb0 = split * p.kb_per;
-  const int kb1 = min(p.kblocks, kb0 + p.kb_per);
-  const int nk = max(0, kb1 - kb0);
-  const int nflush = (nk + kFlushStages - 1) / kFlushStages;
+  // Segment state lives in shared memory (thread 0 writes it at each segment
+  // start) so nothing but the loop index stays live across segments:
+  // [0] tile, [1] kb0, [2] kb1, [3] ring stages and [4] accumulation blocks
+  // consumed by earlier segments, [5] segment count.
+  int* segtab = reinterpret_cast<int*>(tmem_slot + 1);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -104,6 +163,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_empty[b], 128);
     }
     fence_mbar_init();
+    int nseg = 1;  // one (tile, split) unit, or the tiles a stream-K piece touches
+    if (fused) {
+      const int64_t c0 = sk_c(p, blockIdx.x), c1 = sk_c(p, blockIdx.x + 1);
+      nseg = c1 > c0 ? sk_unit_at(p, c1 - 1) - sk_unit_at(p, c0) + 1 : 0;
+    }
+    segtab[3] = 0;
+    segtab[4] = 0;
+    segtab[5] = nseg;
   }
   if (warp == kEpiWarp0) tc::tmem_alloc(tmem_slot, kTmemCols);
   tc::fence_before();
@@ -111,13 +178,47 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
 
+#pragma unroll 1
+  for (int seg = 0; seg < segtab[5]; ++seg) {
+  if (threadIdx.x == 0) {
+    if (fused) {
+      const int64_t c0 = sk_c(p, blockIdx.x), c1 = sk_c(p, blockIdx.x + 1);
+      const int u = sk_unit_at(p, c0) + seg;
+      const int q = u / p.ntiles, t = u - q * p.ntiles;
+      int ib_, jb_;
+      tile_of(t, ib_, jb_);
+      const int wt = ib_ == jb_ ? p.w_diag : p.w_off;
+      const int64_t u0 = sk_u0(p, u), len = sk_len(p, q);
+      segtab[0] = t;
+      segtab[1] = q * p.kb_per + (int)sk_kb(c0, u0, wt, len);
+      segtab[2] = q * p.kb_per + (int)sk_kb(c1, u0, wt, len);
+    } else {
+      const int t = blockIdx.x / p.splits;
+      const int kb0 = (blockIdx.x - t * p.splits) * p.kb_per;
+      segtab[0] = t;
+      segtab[1] = kb0;
+      segtab[2] = min(p.kblocks, kb0 + p.kb_per);
+    }
+  }
+  __syncthreads();
+  const int t = segtab[0], kb0 = segtab[1], kb1 = segtab[2];
+  const int sbase = segtab[3], fbase = segtab[4];
+  double* out = fused ? p.vpart + ((size_t)blockIdx.x * p.max_seg + seg) * 4 * kB
+                      : p.part + (size_t)blockIdx.x * kB * kB;
+  int ib, jb;
+  tile_of(t, ib, jb);
+  const bool diag = ib == jb;
+  const bool share_b = diag && !weighted;  // B operand == A operand
+  const int nk = max(0, kb1 - kb0);
+  const int nflush = (nk + kFlushStages - 1) / kFlushStages;
+
   if (warp == 0) {
     // ---------------------------------------------------------- MMA issuer
     if (tc::elect_one()) {
-      int s = 0;
-      uint32_t ph = 0;
+      int s = sbase % kStages;
+      uint32_t ph = (uint32_t)(sbase / kStages) & 1u;
       int k = 0;
-      for (int f = 0; f < nflush; ++f) {
+      for (int f = fbase; f < fbase + nflush; ++f) {
         const int buf = f & 1;
         mbar_wait(&acc_empty[buf], ((f >> 1) & 1) ^ 1u);
         tc::fence_after();
@@ -220,8 +321,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     OperandChunks r0, r1;
     if (nk > 0) load(0, r0);
     if (nk > 1) load(1, r1);
-    int s = 0;
-    uint32_t ph = 0;
+    int s = sbase % kStages;
+    uint32_t ph = (uint32_t)(sbase / kStages) & 1u;
     for (int k = 0; k < nk; k += 2) {
       mbar_wait(&empty[s], ph ^ 1u);
       store(k, s, r0);
@@ -250,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < 256; c += 32) tc::tmem_st32(lane_base + 256 + c, z);
       tc::tmem_st_wait();
     }
-    for (int f = 0; f < nflush; ++f) {
+    for (int f = fbase; f < fbase + nflush; ++f) {
       const int buf = f & 1;
       mbar_wait(&acc_full[buf], (f >> 1) & 1);
       tc::fence_after();
@@ -274,9 +375,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&acc_empty[buf]);
     }
     // shadow -> global fp64 split partial (row = quad*32 + lane)
-    double* dst = p.part + ((size_t)unit * kB + quad * 32 + lane) * kB;
+    double* dst = out + (size_t)(quad * 32 + lane) * kB;
 #pragma unroll 1
-    for (int c = 0; c < kB && p.vpart == nullptr; c += 16) {
+    for (int c = 0; c < kB && !fused; c += 16) {
       uint32_t sh[32];
       if (nflush > 0) {
         tc::tmem_ld32(lane_base + 256 + (uint32_t)(2 * c), sh);
@@ -292,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          __hiloint2double((int)sh[2 * e + 3], (int)sh[2 * e + 2]));
     }
   }
-  if (p.vpart != nullptr) {
+  if (fused) {
     // Fused epilogue (no N x N Gram in HBM): the fp64 tile goes to SMEM (the
     // operand ring is idle once every role has left its loop; rows padded to
     // kB + 1 doubles for the column pass), then 4 x kB tile sums are written:
@@ -319,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();
     const int tx = threadIdx.x;
-    double* vp = p.vpart + (size_t)unit * 4 * kB;
+    double* vp = out;
     if (tx < kB) {  // row tx of block ib
       double a = 0.0, b = 0.0;
       for (int c = 0; c < kB; ++c) {
@@ -342,7 +443,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       vp[2 * kB + c] = a;
       vp[3 * kB + c] = b;
     }
+    // the next segment's converters reuse the ring, its epilogue the shadow
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (threadIdx.x == 0) {
+      segtab[3] = sbase + nk;
+      segtab[4] = fbase + nflush;
+    }
   }
+  }  // segments
   tc::fence_before();
   __syncthreads();
   if (warp == kEpiWarp0) tc::tmem_dealloc(tmem, kTmemCols);
@@ -350,26 +460,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // row_plain[r] = sum_j G_rj, col_inv[r] = sum_j inv_j G_rj (G symmetric) from
 // the fused tile sums: tiles (I(r), jb >= I(r)) contribute their row sums,
-// tiles (ib < I(r), I(r)) their column sums; splits and tiles in fixed order.
-__global__ void gram_tf32_sums_kernel(const double* __restrict__ vpart, int n, int splits,
-                                      double* __restrict__ row_plain,
+// tiles (ib < I(r), I(r)) their column sums; each tile's segments are read
+// in piece order (= k order) and tiles in fixed order: deterministic.
+__global__ void gram_tf32_sums_kernel(const GramTf32Params p, double* __restrict__ row_plain,
                                       double* __restrict__ col_inv) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < p.n; r += gridDim.x * blockDim.x) {
     const int R = r / kB, o = r - R * kB;
-    const int nb = (n + kB - 1) / kB;
     double a = 0.0, b = 0.0;
-    for (int jb = 0; jb < nb; ++jb) {
+    for (int jb = 0; jb < p.nb; ++jb) {
       const int ib = min(R, jb), jj = max(R, jb);
       const int tile = jj * (jj + 1) / 2 + ib;
       const bool as_row = R <= jb;  // r in the tile's row block
-      for (int s = 0; s < splits; ++s) {
-        const double* vp = vpart + ((size_t)tile * splits + s) * 4 * kB;
-        if (as_row) {
-          a += vp[o];
-          b += vp[kB + o];
-        } else {
-          a += vp[2 * kB + o];
-          b += vp[3 * kB + o];
+      for (int q = 0; q < p.splits; ++q) {
+        const int u = q * p.ntiles + tile;
+        const int b0 = sk_piece_at(p, sk_u0(p, u));
+        const int b1 = sk_piece_at(p, sk_u0(p, u + 1) - 1);
+        for (int pc = b0; pc <= b1; ++pc) {
+          const int64_t c0 = sk_c(p, pc);
+          if (sk_c(p, pc + 1) == c0) continue;  // empty piece
+          const int seg = u - sk_unit_at(p, c0);
+          const double* vp = p.vpart + ((size_t)pc * p.max_seg + seg) * 4 * kB;
+          if (as_row) {
+            a += vp[o];
+            b += vp[kB + o];
+          } else {
+            a += vp[2 * kB + o];
+            b += vp[3 * kB + o];
+          }
         }
       }
     }
@@ -398,7 +515,22 @@ __global__ void gram_tf32_reduce_kernel(const double* __restrict__ part, int n, 
 struct Plan {
   int nb, ntiles, splits, kblocks, kb_per, units;
   size_t smem, ws;
+  // fused sums (stream-K)
+  int pieces, max_seg, w_off, w_diag;
+  int64_t total;
 };
+
+// Relative cost of a shared-operand diagonal tile (off-diagonal = 10).  It
+// loads half the bytes but runs the same MMAs: measured at 1000 x 256^3,
+// costs 0.6 / 0.7 / 0.8 / 1.0 gave 153.8 / 144.2 / 146.5 / 149.6 ms (0.5:
+// 183.9 ms).  PIDB_K1_DIAG_COST in (0, 1] overrides the default 0.7.
+int diag_cost10() {
+  if (const char* e = std::getenv("PIDB_K1_DIAG_COST")) {
+    const double x = std::atof(e);
+    if (x > 0.0 && x <= 1.0) return std::max(1, (int)std::lround(10.0 * x));
+  }
+  return 7;
+}
 
 Plan plan(int64_t n, int64_t m) {
   Plan g{};
@@ -415,6 +547,26 @@ Plan plan(int64_t n, int64_t m) {
   return g;
 }
 
+// Stream-K partition of the fused-sums launch: one piece per SM.
+Plan plan_sums(int64_t n, int64_t m, bool weighted) {
+  Plan g = plan(n, m);
+  g.w_off = 10;
+  g.w_diag = weighted ? 10 : diag_cost10();
+  GramTf32Params p{};
+  p.nb = g.nb; p.ntiles = g.ntiles; p.splits = g.splits; p.kblocks = g.kblocks;
+  p.kb_per = g.kb_per; p.w_off = g.w_off; p.w_diag = g.w_diag;
+  g.total = p.total = sk_u0(p, (int64_t)g.splits * g.ntiles);
+  g.pieces = p.pieces = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), g.total));
+  if (g.total > INT64_MAX / (g.pieces + 1)) g.pieces = 0;  // rejected by the entry point
+  g.max_seg = 1;
+  for (int b = 0; b < g.pieces; ++b) {
+    const int64_t c0 = sk_c(p, b), c1 = sk_c(p, b + 1);
+    if (c1 > c0) g.max_seg = std::max(g.max_seg, sk_unit_at(p, c1 - 1) - sk_unit_at(p, c0) + 1);
+  }
+  g.ws = 256 + (size_t)g.pieces * g.max_seg * 4 * kB * sizeof(double);
+  return g;
+}
+
 }  // namespace
 }  // namespace pidb
 
@@ -422,7 +574,7 @@ using namespace pidb;
 
 extern "C" size_t pidb_gram_tf32x3_workspace_bytes(int64_t n, int64_t m) {
   if (n < 1 || m < 1) return 0;
-  return plan(n, m).ws;
+  return std::max(plan(n, m).ws, std::max(plan_sums(n, m, false).ws, plan_sums(n, m, true).ws));
 }
 
 extern "C" int pidb_gram_tf32x3_sums(const float* u, int64_t n, int64_t m, int64_t ld,
@@ -433,20 +585,22 @@ extern "C" int pidb_gram_tf32x3_sums(const float* u, int64_t n, int64_t m, int64
   PIDB_REQUIRE(ld >= m && (ld * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(u) & 15) == 0,
                "member rows must be 16-byte aligned with ld >= m");
   PIDB_REQUIRE(n <= (1 << 16), "too many members for the dense Gram");
-  const Plan g = plan(n, m);
+  const Plan g = plan_sums(n, m, w != nullptr);
+  PIDB_REQUIRE(g.pieces > 0, "ensemble too large for the fused Gram sums");
   PIDB_REQUIRE(ws && ws_bytes >= g.ws, "workspace too small: need %zu bytes", g.ws);
   GramTf32Params p{};
   p.n = (int)n; p.nb = g.nb; p.ntiles = g.ntiles; p.splits = g.splits; p.kblocks = g.kblocks;
   p.kb_per = g.kb_per; p.m = m; p.ld = ld; p.u = u; p.w = w;
   p.inv = inv;
   p.vpart = reinterpret_cast<double*>(static_cast<char*>(ws) + 256);
+  p.pieces = g.pieces; p.max_seg = g.max_seg; p.w_off = g.w_off; p.w_diag = g.w_diag;
+  p.total = g.total;
   cudaStream_t st = (cudaStream_t)stream;
   PIDB_CUDA(cudaFuncSetAttribute(gram_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)g.smem));
-  gram_tf32_kernel<<<g.units, kThreads, g.smem, st>>>(p);
+  gram_tf32_kernel<<<g.pieces, kThreads, g.smem, st>>>(p);
   PIDB_LAUNCH_CHECK("gram_tf32_kernel (fused sums)");
-  gram_tf32_sums_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p.vpart, (int)n, g.splits,
-                                                                      row_plain, col_inv);
+  gram_tf32_sums_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p, row_plain, col_inv);
   PIDB_LAUNCH_CHECK("gram_tf32_sums_kernel");
   return PIDB_OK;
 }

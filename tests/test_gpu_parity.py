@@ -81,6 +81,40 @@ def test_fuzzy_gram_3xtf32(pb, n, m, weighted):
     assert np.array_equal(got, got.T)
 
 
+@pytest.mark.parametrize("n,m,weighted", [(3, 5, False), (5, 40, True), (129, 777, False),
+                                          (300, 5000, True), (1100, 3000, False),
+                                          (2200, 1500, False), (2200, 700, True)])
+def test_fused_gram_sums_stream_k(pb, n, m, weighted):
+    """K1 fused sums (stream-K pieces: a piece spans k-ranges of several
+    tiles, up to 171 tiles on 148 pieces here, and tiny m leaves empty
+    pieces): row sums of G and inverse-mass-weighted column sums vs the fp64
+    product, 1e-5 relative (3xTF32 bound); bit-identical on a repeat call."""
+    from paper_2512_15187_b200 import _native as N
+    from paper_2512_15187_b200.depth import _launch
+
+    U, w = make_fuzzy(n * 7 + m, n, (m,), weighted)
+    de = pb.stage(pb.Ensemble(pb.GridSpec((m,), w), [pb.ProbMask(pb.GridSpec((m,), w), u) for u in U]))
+    inv_h = 1.0 / (1.0 + np.arange(n, dtype=np.float64))
+    inv = torch.tensor(inv_h, device=de.device)
+    ws = de.workspace(N.load().pidb_gram_tf32x3_workspace_bytes(n, de.m))
+
+    def run():
+        rc = torch.zeros(2 * n, dtype=torch.float64, device=de.device)
+        _launch("pidb_gram_tf32x3_sums", de.ptr(), n, de.m, de.ld, de.wptr(), inv.data_ptr(),
+                rc.data_ptr(), rc.data_ptr() + 8 * n, ws.data_ptr(), ws.numel(),
+                torch.cuda.current_stream(de.device).cuda_stream)
+        return rc.cpu().numpy()
+
+    got = run()
+    X = U.astype(np.float64)
+    G = (X * (w if weighted else 1.0)) @ X.T
+    for a, b in ((got[:n], G.sum(1)), (got[n:], G @ inv_h)):
+        err = np.abs(a - b).max() / np.abs(b).max()
+        print(f"fused sums n={n} m={m} weighted={weighted}: max rel err {err:.3e}")
+        assert err < 1e-5
+    assert np.array_equal(run(), got)
+
+
 @pytest.mark.parametrize("n,res", [(300, 24), (1000, 32)])
 def test_pid_gram_within_bound(pb, n, res):
     """PID from the tensor-core Gram vs the exact fp64 O(N*M) path on ellipsoid
