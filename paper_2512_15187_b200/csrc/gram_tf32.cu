@@ -523,7 +523,8 @@ struct Plan {
 // Relative cost of a shared-operand diagonal tile (off-diagonal = 10).  It
 // loads half the bytes but runs the same MMAs: measured at 1000 x 256^3,
 // costs 0.6 / 0.7 / 0.8 / 1.0 gave 153.8 / 144.2 / 146.5 / 149.6 ms (0.5:
-// 183.9 ms).  PIDB_K1_DIAG_COST in (0, 1] overrides the default 0.7.
+// 183.9 ms; box-to-box spread is of the same order).  PIDB_K1_DIAG_COST in
+// (0, 1] overrides the default 0.7.
 int diag_cost10() {
   if (const char* e = std::getenv("PIDB_K1_DIAG_COST")) {
     const double x = std::atof(e);
@@ -556,7 +557,9 @@ Plan plan_sums(int64_t n, int64_t m, bool weighted) {
   p.nb = g.nb; p.ntiles = g.ntiles; p.splits = g.splits; p.kblocks = g.kblocks;
   p.kb_per = g.kb_per; p.w_off = g.w_off; p.w_diag = g.w_diag;
   g.total = p.total = sk_u0(p, (int64_t)g.splits * g.ntiles);
-  g.pieces = p.pieces = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), g.total));
+  int pieces = sm_count();
+  if (const char* e = std::getenv("PIDB_K1_PIECES")) pieces = std::max(1, std::atoi(e));  // A/B hook
+  g.pieces = p.pieces = (int)std::max<int64_t>(1, std::min<int64_t>(pieces, g.total));
   if (g.total > INT64_MAX / (g.pieces + 1)) g.pieces = 0;  // rejected by the entry point
   g.max_seg = 1;
   for (int b = 0; b < g.pieces; ++b) {
