@@ -137,22 +137,26 @@ __global__ void __launch_bounds__(kGramThreads, 1)
   if (warp == 2) tc::tmem_dealloc(tmem, kBN);
 }
 
-// I[i][j] = I[j][i] = sum over splits of the tile holding (min, max).
+// I[i][j] = I[j][i] = sum over splits of the tile holding (i, j), i <= j.
+// Each upper-triangle entry is summed once (reads coalesced along j) and
+// written to both halves; int64 sums are exact, so the order is immaterial.
 __global__ void gram_i8_reduce_kernel(const int32_t* __restrict__ part, int n, int nib,
                                       int splits, int64_t* __restrict__ out) {
   const int64_t total = (int64_t)n * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int a = (int)(e / n), b = (int)(e - (int64_t)a * n);
-    const int i = min(a, b), j = max(a, b);
+    const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
+    if (i > j) continue;
     const int ib = i / kBM, jb = j / kBN;
     int t = 0;
     for (int q = 0; q < jb; ++q) t += min(nib, 2 * q + 2);
     t += ib;
     const int32_t* src = part + ((size_t)t * splits * kBM + (i - ib * kBM)) * kBN + (j - jb * kBN);
     int64_t acc = 0;
-    for (int s = 0; s < splits; ++s) acc += src[(size_t)s * kBM * kBN];
+#pragma unroll 8
+    for (int s = 0; s < splits; ++s) acc += __ldg(src + (size_t)s * kBM * kBN);
     out[e] = acc;
+    if (i != j) out[(int64_t)j * n + i] = acc;
   }
 }
 
