@@ -495,20 +495,24 @@ __global__ void gram_tf32_sums_kernel(const GramTf32Params p, double* __restrict
   }
 }
 
-// G[i][j] = G[j][i] = sum over splits (fixed order) of the tile holding (min, max).
+// G[i][j] = G[j][i] = sum over splits (fixed order) of the tile holding
+// (i, j), i <= j: each upper-triangle entry is summed once along coalesced
+// rows and written to both halves.
 __global__ void gram_tf32_reduce_kernel(const double* __restrict__ part, int n, int splits,
                                         double* __restrict__ out) {
   const int64_t total = (int64_t)n * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int a = (int)(e / n), b = (int)(e - (int64_t)a * n);
-    const int i = min(a, b), j = max(a, b);
+    const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
+    if (i > j) continue;
     const int ib = i / kB, jb = j / kB;
     const int t = jb * (jb + 1) / 2 + ib;
     const double* src = part + ((size_t)t * splits * kB + (i - ib * kB)) * kB + (j - jb * kB);
     double acc = 0.0;
-    for (int s = 0; s < splits; ++s) acc += src[(size_t)s * kB * kB];
+#pragma unroll 4
+    for (int s = 0; s < splits; ++s) acc += __ldg(src + (size_t)s * kB * kB);
     out[e] = acc;
+    if (i != j) out[(int64_t)j * n + i] = acc;
   }
 }
 
