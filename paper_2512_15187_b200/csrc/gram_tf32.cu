@@ -460,36 +460,45 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // row_plain[r] = sum_j G_rj, col_inv[r] = sum_j inv_j G_rj (G symmetric) from
 // the fused tile sums: tiles (I(r), jb >= I(r)) contribute their row sums,
-// tiles (ib < I(r), I(r)) their column sums; each tile's segments are read
-// in piece order (= k order) and tiles in fixed order: deterministic.
+// tiles (ib < I(r), I(r)) their column sums; a unit's segments are read in
+// piece order (= k order).
 __global__ void gram_tf32_sums_kernel(const GramTf32Params p, double* __restrict__ row_plain,
                                       double* __restrict__ col_inv) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < p.n; r += gridDim.x * blockDim.x) {
-    const int R = r / kB, o = r - R * kB;
-    double a = 0.0, b = 0.0;
-    for (int jb = 0; jb < p.nb; ++jb) {
-      const int ib = min(R, jb), jj = max(R, jb);
-      const int tile = jj * (jj + 1) / 2 + ib;
-      const bool as_row = R <= jb;  // r in the tile's row block
-      for (int q = 0; q < p.splits; ++q) {
-        const int u = q * p.ntiles + tile;
-        const int b0 = sk_piece_at(p, sk_u0(p, u));
-        const int b1 = sk_piece_at(p, sk_u0(p, u + 1) - 1);
-        for (int pc = b0; pc <= b1; ++pc) {
-          const int64_t c0 = sk_c(p, pc);
-          if (sk_c(p, pc + 1) == c0) continue;  // empty piece
-          const int seg = u - sk_unit_at(p, c0);
-          const double* vp = p.vpart + ((size_t)pc * p.max_seg + seg) * 4 * kB;
-          if (as_row) {
-            a += vp[o];
-            b += vp[kB + o];
-          } else {
-            a += vp[2 * kB + o];
-            b += vp[3 * kB + o];
-          }
-        }
+  // one warp per member row; lanes take the (column block, K round) units in
+  // a fixed assignment and a fixed shuffle tree combines them: deterministic
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= p.n) return;
+  const int R = r / kB, o = r - R * kB;
+  double a = 0.0, b = 0.0;
+  for (int idx = lane; idx < p.nb * p.splits; idx += 32) {
+    const int jb = idx / p.splits, q = idx - jb * p.splits;
+    const int ib = min(R, jb), jj = max(R, jb);
+    const int tile = jj * (jj + 1) / 2 + ib;
+    const bool as_row = R <= jb;  // r in the tile's row block
+    const int u = q * p.ntiles + tile;
+    const int b0 = sk_piece_at(p, sk_u0(p, u));
+    const int b1 = sk_piece_at(p, sk_u0(p, u + 1) - 1);
+    for (int pc = b0; pc <= b1; ++pc) {
+      const int64_t c0 = sk_c(p, pc);
+      if (sk_c(p, pc + 1) == c0) continue;  // empty piece
+      const int seg = u - sk_unit_at(p, c0);
+      const double* vp = p.vpart + ((size_t)pc * p.max_seg + seg) * 4 * kB;
+      if (as_row) {
+        a += vp[o];
+        b += vp[kB + o];
+      } else {
+        a += vp[2 * kB + o];
+        b += vp[3 * kB + o];
       }
     }
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, s);
+    b += __shfl_xor_sync(0xffffffffu, b, s);
+  }
+  if (lane == 0) {
     row_plain[r] = a;
     col_inv[r] = b;
   }
@@ -607,7 +616,7 @@ extern "C" int pidb_gram_tf32x3_sums(const float* u, int64_t n, int64_t m, int64
                                  (int)g.smem));
   gram_tf32_kernel<<<g.pieces, kThreads, g.smem, st>>>(p);
   PIDB_LAUNCH_CHECK("gram_tf32_kernel (fused sums)");
-  gram_tf32_sums_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(p, row_plain, col_inv);
+  gram_tf32_sums_kernel<<<(unsigned)((n + 3) / 4), 128, 0, st>>>(p, row_plain, col_inv);
   PIDB_LAUNCH_CHECK("gram_tf32_sums_kernel");
   return PIDB_OK;
 }
