@@ -294,24 +294,11 @@ __device__ __forceinline__ long long dkey(double d) {
   long long b = __double_as_longlong(d);
   return b >= 0 ? b : (b ^ 0x7FFFFFFFFFFFFFFFLL);
 }
-template <typename T>
-__global__ void validate_kernel(T* __restrict__ u, int64_t n, int64_t m, int64_t ld, int clamp,
-                                unsigned long long* __restrict__ nonfinite,
-                                long long* __restrict__ kmin, long long* __restrict__ kmax) {
-  unsigned long long bad = 0;
-  double lo = 0.0, hi = 0.0;
-  bool any = false;
-  for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m;
-       x += (int64_t)gridDim.x * blockDim.x) {
-    T v = u[i * ld + x];
-    const double d = (double)v;
-    if (!isfinite(d)) { ++bad; continue; }
-    if (!any) { lo = hi = d; any = true; }
-    lo = fmin(lo, d);
-    hi = fmax(hi, d);
-    if (clamp && (d < 0.0 || d > 1.0)) u[i * ld + x] = d < 0.0 ? T(0) : T(1);
-  }
+// Warp-combine one thread's (non-finite count, finite min/max) and publish
+// with one set of atomics per warp.
+__device__ __forceinline__ void validate_reduce(unsigned long long bad, double lo, double hi,
+                                                bool any, unsigned long long* nonfinite,
+                                                long long* kmin, long long* kmax) {
   for (int o = 16; o > 0; o >>= 1) {
     bad += __shfl_xor_sync(0xffffffffu, bad, o);
     const double l2 = __shfl_xor_sync(0xffffffffu, lo, o);
@@ -331,6 +318,62 @@ __global__ void validate_kernel(T* __restrict__ u, int64_t n, int64_t m, int64_t
     }
   }
 }
+
+template <typename T>
+__global__ void validate_kernel(T* __restrict__ u, int64_t n, int64_t m, int64_t ld, int clamp,
+                                unsigned long long* __restrict__ nonfinite,
+                                long long* __restrict__ kmin, long long* __restrict__ kmax) {
+  unsigned long long bad = 0;
+  double lo = 0.0, hi = 0.0;
+  bool any = false;
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    T v = u[i * ld + x];
+    const double d = (double)v;
+    if (!isfinite(d)) { ++bad; continue; }
+    if (!any) { lo = hi = d; any = true; }
+    lo = fmin(lo, d);
+    hi = fmax(hi, d);
+    if (clamp && (d < 0.0 || d > 1.0)) u[i * ld + x] = d < 0.0 ? T(0) : T(1);
+  }
+  validate_reduce(bad, lo, hi, any, nonfinite, kmin, kmax);
+}
+
+// fp32 members with 16-byte aligned rows: 128-bit loads, min/max in float
+// (exact: the float extremes convert to the same doubles).
+__global__ void validate_f32x4_kernel(float* __restrict__ u, int64_t n, int64_t m, int64_t ld,
+                                      int clamp, unsigned long long* __restrict__ nonfinite,
+                                      long long* __restrict__ kmin, long long* __restrict__ kmax) {
+  unsigned long long bad = 0;
+  float lo = 0.f, hi = 0.f;
+  bool any = false;
+  const int64_t m4 = m >> 2;
+  auto visit = [&](float& v, bool& dirty) {
+    if (!isfinite(v)) { ++bad; return; }
+    if (!any) { lo = hi = v; any = true; }
+    lo = fminf(lo, v);
+    hi = fmaxf(hi, v);
+    if (clamp && (v < 0.f || v > 1.f)) { v = v < 0.f ? 0.f : 1.f; dirty = true; }
+  };
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
+    float* row = u + i * ld;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m4;
+         x += (int64_t)gridDim.x * blockDim.x) {
+      float4 v = reinterpret_cast<const float4*>(row)[x];
+      bool dirty = false;
+      visit(v.x, dirty); visit(v.y, dirty); visit(v.z, dirty); visit(v.w, dirty);
+      if (dirty) reinterpret_cast<float4*>(row)[x] = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (m & 3)) {
+      float v = row[(m4 << 2) + threadIdx.x];
+      bool dirty = false;
+      visit(v, dirty);
+      if (dirty) row[(m4 << 2) + threadIdx.x] = v;
+    }
+  }
+  validate_reduce(bad, (double)lo, (double)hi, any, nonfinite, kmin, kmax);
+}
 }  // namespace
 }  // namespace pidb
 
@@ -345,7 +388,12 @@ extern "C" int pidb_validate(void* u, int dtype, int64_t n, int64_t m, int64_t l
   PIDB_CUDA(cudaMemcpyAsync(stats, init, sizeof(init), cudaMemcpyHostToDevice, st));
   const dim3 blocks((unsigned)std::min<int64_t>((m + 255) / 256, 64),
                     (unsigned)std::min<int64_t>(n, 1024));
-  if (dtype == PIDB_F32)
+  if (dtype == PIDB_F32 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(u) & 15) == 0) {
+    const dim3 b4((unsigned)std::min<int64_t>((m / 4 + 255) / 256, 64),
+                  (unsigned)std::min<int64_t>(n, 1024));
+    validate_f32x4_kernel<<<b4.x ? b4 : dim3(1, b4.y), 256, 0, st>>>(static_cast<float*>(u), n,
+                                                                     m, ld, clamp, nf, kmin, kmax);
+  } else if (dtype == PIDB_F32)
     validate_kernel<float><<<blocks, 256, 0, st>>>(static_cast<float*>(u), n, m, ld, clamp, nf,
                                                    kmin, kmax);
   else

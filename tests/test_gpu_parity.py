@@ -632,3 +632,40 @@ def test_cluster_fallback(pb, monkeypatch):
     got = pb.depth_pid(e)
     close(got.depth, want.depth, 1e-13)
     np.testing.assert_array_equal(got.rank, want.rank)
+
+
+@pytest.mark.parametrize("n,m,ld", [(1, 1, 4), (3, 3, 4), (2, 5, 8), (7, 1027, 1028), (3, 12290, 12320),
+                                    (4, 1027, 1027), (2, 7, 7)])
+@pytest.mark.parametrize("clamp", [False, True])
+def test_validate_kernel_stats(pb, n, m, ld, clamp):
+    """pidb_validate (vectorised when ld % 4 == 0, scalar otherwise): the
+    non-finite count, the finite min / max and the in-place [0, 1] clip match
+    numpy, including the m % 4 tail cells and the padding beyond m untouched."""
+    from paper_2512_15187_b200 import _native as N
+    from paper_2512_15187_b200.device import _key_to_double
+
+    rng = np.random.default_rng(n * 131 + m + ld)
+    buf = rng.uniform(-1e-7, 1.0 + 1e-7, size=(n, ld)).astype(np.float32)
+    buf[:, m:] = 7.0  # padding: must be neither read nor written
+    live = buf[:, :m]
+    k = max(1, live.size // 50)
+    idx = rng.choice(live.size, size=min(k, live.size), replace=False)
+    bad = idx[: len(idx) // 2] if live.size > 1 else idx[:0]
+    live.flat[bad] = rng.choice([np.nan, np.inf, -np.inf], size=bad.size)
+    t = torch.tensor(buf, device="cuda")
+    stats = torch.empty(3, dtype=torch.int64, device="cuda")
+    N.call("pidb_validate", t.data_ptr(), N.PIDB_F32, n, m, ld, int(clamp), stats.data_ptr(),
+           torch.cuda.current_stream().cuda_stream)
+    nf, kmin, kmax = (int(v) for v in stats.cpu().tolist())
+    fin = live[np.isfinite(live)]
+    assert nf == int((~np.isfinite(live)).sum())
+    if fin.size:
+        assert _key_to_double(kmin) == float(fin.min())
+        assert _key_to_double(kmax) == float(fin.max())
+    got = t.cpu().numpy()
+    want = buf.copy()
+    if clamp:
+        w = want[:, :m]
+        fmask = np.isfinite(w)
+        w[fmask] = np.clip(w[fmask], 0.0, 1.0)
+    np.testing.assert_array_equal(got, want)
