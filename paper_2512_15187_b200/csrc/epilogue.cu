@@ -144,13 +144,17 @@ __device__ __forceinline__ uint64_t eid_term_bits53(int64_t m_i, int64_t inter) 
 // masses m_j = I_jj staged per block in shared memory (one strided read per
 // block instead of one per warp).
 constexpr int kDiagChunk = 1024;
+constexpr int kEidWarpsPerRow = 4;  // 4 warps share a row: 4x the warps in flight
 __global__ void eid_exact_kernel(const int64_t* __restrict__ g, int64_t n,
                                  double* __restrict__ in_in, double* __restrict__ in_out,
                                  double* __restrict__ depth, double* __restrict__ mass) {
   __shared__ int64_t sdiag[kDiagChunk];
-  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-  for (int64_t base = (int64_t)blockIdx.x * wpb; base < n; base += (int64_t)gridDim.x * wpb) {
-    const int64_t i = base + (threadIdx.x >> 5);
+  __shared__ unsigned __int128 spart[2][32];  // per-warp (row, col) sums, <= 32 warps
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rpb = (blockDim.x >> 5) / kEidWarpsPerRow;  // rows per block
+  const int sub = warp % kEidWarpsPerRow;
+  for (int64_t base = (int64_t)blockIdx.x * rpb; base < n; base += (int64_t)gridDim.x * rpb) {
+    const int64_t i = base + warp / kEidWarpsPerRow;
     const bool live = i < n;
     const int64_t mi = live ? g[i * n + i] : 0;
     unsigned __int128 row = 0, col = 0;
@@ -161,7 +165,7 @@ __global__ void eid_exact_kernel(const int64_t* __restrict__ g, int64_t n,
       __syncthreads();
       if (live) {
         const int64_t* gi = g + i * n + j0;
-        for (int t = lane; t < cnt; t += 32) {
+        for (int t = sub * 32 + lane; t < cnt; t += 32 * kEidWarpsPerRow) {
           const int64_t gij = gi[t];
           row += eid_term_bits53(mi, gij);
           col += eid_term_bits53(sdiag[t], gij);
@@ -177,7 +181,17 @@ __global__ void eid_exact_kernel(const int64_t* __restrict__ g, int64_t n,
       row += ((unsigned __int128)rh << 64) | rl;
       col += ((unsigned __int128)ch << 64) | cl;
     }
-    if (live && lane == 0) {
+    if (lane == 0) {
+      spart[0][warp] = row;
+      spart[1][warp] = col;
+    }
+    __syncthreads();
+    if (live && lane == 0 && sub == 0) {
+      // integer sums: exact in any order
+      for (int s = 1; s < kEidWarpsPerRow; ++s) {
+        row += spart[0][warp + s];
+        col += spart[1][warp + s];
+      }
       if (mass) mass[i] = (double)mi;  // |C_i|, exact
       const double rs = __dmul_rn(u128_to_double_rn(row), 1.1102230246251565e-16);  // 2^-53
       const double cs = __dmul_rn(u128_to_double_rn(col), 1.1102230246251565e-16);
@@ -255,7 +269,8 @@ extern "C" int pidb_eid_exact_epilogue(const int64_t* gram, int64_t n, double* i
                                        double* mass, void* stream) {
   PIDB_REQUIRE(n >= 1 && gram && in_in && in_out && depth, "bad arguments to pidb_eid_exact_epilogue");
   cudaStream_t st = (cudaStream_t)stream;
-  eid_exact_kernel<<<blocks_for(n, 8), 256, 0, st>>>(gram, n, in_in, in_out, depth, mass);
+  eid_exact_kernel<<<blocks_for(n, 256 / 32 / kEidWarpsPerRow), 256, 0, st>>>(gram, n, in_in,
+                                                                              in_out, depth, mass);
   PIDB_LAUNCH_CHECK("eid_exact_kernel");
   return launch_ranks(n, depth, rank, st);
 }
