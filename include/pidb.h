@@ -142,6 +142,18 @@ int pidb_gram_tf32x3_sums(const float* u, int64_t n, int64_t m, int64_t ld,
                           const double* w, const double* inv, double* row_plain,
                           double* col_inv, void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------ K1-f64 ----
+ * gram_block seam (reduction.py:75-97) in fp64 on the CUDA cores:
+ *   out[i*nc+j] = sum_x w(x) rows[i,x] * c(j,x),  c = cols or 1 - cols
+ * rows (nr, ldr) and cols (nc, ldc) of dtype PIDB_F32 or PIDB_F64 (both the
+ * same), w nullable; fp64 products and sums (the reference's contract, its
+ * tests use rtol 1e-12, tests/test_reduction.py:46-66).  Deterministic
+ * split-K with a fixed-order reduction; workspace needs no initialisation. */
+size_t pidb_gram_f64_workspace_bytes(int64_t nr, int64_t nc, int64_t m);
+int pidb_gram_f64(const void* rows, const void* cols, int dtype, int64_t nr,
+                  int64_t nc, int64_t m, int64_t ldr, int64_t ldc, const double* w,
+                  int complement, double* out, void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- K4 ----
  * Gram -> (row_plain, col_inv): row_plain[i] = sum_j G[i,j],
  * col_inv[j] = sum_i inv[i] G[i,j]  (depth.py:155-160). */

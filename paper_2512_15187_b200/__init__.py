@@ -10,7 +10,6 @@ kernels in ``libpidb.so`` (C ABI: include/pidb.h).  No CPU fallback.
 from .depth import (
     CV_WARN_THRESHOLD,
     METHOD_NAMES,
-    TILE_BYTES,
     DepthResult,
     compare_pid_vs_mean,
     depth_by_method,
@@ -48,7 +47,7 @@ from .inclusion import fuzzy_dice, prob_inclusion, prob_iou, subset_epsilon
 from .reduction import gram_block
 from .synth import (gen_contour_ensemble_2d, gen_disk_ensemble, gen_ellipsoid_ensemble,
                     gen_fuzzy_disk)
-from .fuzzify import ScalarField, default_width, fuzzy_isocontour, hard_isocontour, normalize_density
+from .io import ScalarField
 from .boxplot import Band, BoxplotArtifact, build_boxplot, emit_slice_images, write_pgm
 from .consistency import RankScatter, kendall_tau, pearson, rank_scatter, stability_test
 from .io import (manifest_guarantees_binary, read_depth_csv, read_manifest, read_volume,
@@ -63,13 +62,9 @@ __all__ = [
     "RankScatter",
     "ScalarField",
     "build_boxplot",
-    "default_width",
     "emit_slice_images",
-    "fuzzy_isocontour",
-    "hard_isocontour",
     "kendall_tau",
     "manifest_guarantees_binary",
-    "normalize_density",
     "pearson",
     "rank_scatter",
     "read_depth_csv",
@@ -96,7 +91,6 @@ __all__ = [
     "ManifestError",
     "METHOD_NAMES",
     "ProbMask",
-    "TILE_BYTES",
     "ValidationError",
     "VolumeFormatError",
     "binarize",

@@ -57,6 +57,9 @@ SIGNATURES: dict[str, tuple] = {
     "pidb_gram_tf32x3_workspace_bytes": (_sz, [_i64, _i64]),
     "pidb_gram_tf32x3": (_int, [_p, _i64, _i64, _i64, _p, _p, _p, _sz, _p]),
     "pidb_gram_reduce": (_int, [_p, _i64, _p, _p, _p, _p]),
+    "pidb_gram_f64_workspace_bytes": (_sz, [_i64, _i64, _i64]),
+    "pidb_gram_f64": (_int, [_p, _p, _int, _i64, _i64, _i64, _i64, _i64, _p, _int, _p, _p, _sz,
+                             _p]),
     "pidb_depth_epilogue": (_int, [_int, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "pidb_inverse_masses": (_int, [_i64, _p, _p, _p]),
     "pidb_eid_exact_epilogue": (_int, [_p, _i64, _p, _p, _p, _p, _p, _p]),
@@ -74,10 +77,6 @@ SIGNATURES: dict[str, tuple] = {
     "pidb_gram_tf32x3_sums": (_int, [_p, _i64, _i64, _i64, _p, _p, _p, _p, _p, _sz, _p]),
     "pidb_band_envelopes": (_int, [_p, _int, _i64, _i64, _i64, _p, _i64, _dbl, _p, _int, _p, _p,
                                    _p]),
-}
-
-# Entry points declared in pidb.h whose kernels are still being brought up.
-_NOT_YET_BUILT = {
 }
 
 _lib = None
@@ -106,7 +105,6 @@ def load(path: Path | str | None = None) -> C.CDLL:
                 continue
             fn.restype = res
             fn.argtypes = args
-        missing = [m for m in missing if m not in _NOT_YET_BUILT]
         if missing:
             raise ImportError(f"{p} lacks symbols {missing}")
         if lib.pidb_abi_version() != 1:

@@ -32,7 +32,6 @@ from . import _native as N
 from .device import DeviceEnsemble, stage, stream_ptr
 from .errors import DegenerateEnsembleError, ValidationError
 
-TILE_BYTES = 32 * 2**20          # depth.py:36 (API parity; tiling is on-device here)
 CV_WARN_THRESHOLD = 0.5          # depth.py:40
 METHOD_NAMES = ("eid", "pid", "pid-mean", "dice", "iou")  # depth.py:42
 PID_ALGORITHMS = ("auto", "gram", "factorized")
@@ -129,22 +128,30 @@ _GRAPHS = os.environ.get("PIDB_GRAPHS", "1") != "0"
 _GRAPH_LOCK = threading.RLock()
 
 
-def _graphed(de: DeviceEnsemble, key: str, enqueue):
-    """Queue the device work of one call; returns enqueue()'s output tensors.
+def _graphed(de: DeviceEnsemble, key: str, enqueue) -> "_Out":
+    """Queue the device work of one call and return its result block, already
+    copied to the host.  ``enqueue()`` returns the call's ``_Out``.
 
     A DeviceEnsemble reused for the same method runs eagerly once (plans,
     workspaces), is captured into a CUDA graph on its second call and
     replayed afterwards: one graph launch instead of the ctypes launches and
     allocations of the eager path (the small configurations are
-    launch-bound).  Sharded ensembles (NCCL in the sequence) and timed runs
-    (KERNEL_EVENTS) stay eager."""
+    launch-bound).  Graphs are cached per (method, stream): a graph owns its
+    workspace (completion counters), so two threads replaying on different
+    streams never share one.  Replay and the D2H of the graph's result block
+    run under the graph's own lock, so a caller always reads the block its
+    own replay wrote.  Sharded ensembles (NCCL in the sequence) and timed
+    runs (KERNEL_EVENTS) stay eager."""
     if not _GRAPHS or de.sharded or KERNEL_EVENTS is not None:
-        return enqueue()
+        out = enqueue()
+        out.host()
+        return out
+    skey = (key, torch.cuda.current_stream(de.device).cuda_stream)
     with _GRAPH_LOCK:
         cache = de._cache.setdefault("graphs", {})
-        ent = cache.get(key)
+        ent = cache.get(skey)
         if ent is None:
-            cache[key] = False
+            cache[skey] = False
         elif ent is False:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, capture_error_mode="thread_local"):
@@ -152,12 +159,17 @@ def _graphed(de: DeviceEnsemble, key: str, enqueue):
             for ws in de._cache.pop("graph_ws_pending", []):
                 ws.zero_()  # the kernels leave their counters at zero after each replay
                 de._cache.setdefault("graph_ws", []).append(ws)
-            ent = cache[key] = (g, outs)
+            ent = cache[skey] = (g, outs, threading.Lock())
     if ent is None:
-        return enqueue()
-    g, outs = ent
-    g.replay()
-    return outs
+        out = enqueue()
+        out.host()
+        return out
+    g, outs, lock = ent
+    with lock:
+        g.replay()
+        out = outs.fresh()
+        out.host()  # D2H (synchronises the stream) before the next replay
+    return out
 
 
 def _f64(n: int, dev) -> torch.Tensor:
@@ -283,11 +295,22 @@ def member_masses(ensemble, workers: int | None = None, require_binary: bool = F
     return mass.cpu().numpy()
 
 
-def _raise_first_nonbinary(de: DeviceEnsemble, nb: torch.Tensor) -> None:
-    bad = np.flatnonzero(nb.cpu().numpy())
+def _raise_first_nonbinary(de: DeviceEnsemble, nb) -> None:
+    bad = np.flatnonzero(nb.cpu().numpy() if isinstance(nb, torch.Tensor) else nb)
     if bad.size:
         i = int(bad[0])
         raise ValidationError(f"member {de.ids[i]!r} is not binary (0/1) valued")
+
+
+def _member_mean_terms(values, mean_values, weights) -> tuple[float, float]:
+    """Seam of depth.py:231-243: fused (sum w u mean, sum w u) for one member
+    against the mean mask, one device pass with fp64 accumulation (K8).  The
+    depth methods themselves never call it: K5 forms these sums for every
+    member in the same pass that forms the mean."""
+    from .inclusion import _pair
+
+    num, mass = _pair(values, mean_values, weights, N.PIDB_OP_INCLUSION)
+    return num, mass
 
 
 def depth_pid_mean(ensemble, workers: int | None = None,
@@ -309,10 +332,9 @@ def depth_pid_mean(ensemble, workers: int | None = None,
         inv, ii, io, d = out.ptrs()
         N.call("pidb_depth_epilogue", N.PIDB_EPI_PID_MEAN, n, p, p + 8 * n, p + 16 * n,
                inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
-        return buf, out
+        return out
 
-    _, out = _graphed(de, "pid-mean", enqueue)
-    out = out.fresh()
+    out = _graphed(de, "pid-mean", enqueue)
     host = out.host_extra()[n:]
     masses, col_mean = host[:n], float(host[n])
     if col_mean == 0.0:
@@ -392,10 +414,10 @@ def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") 
     else:
         def enqueue():
             out = _Out(n, de.device, extra=2 * n + 1)
-            return _pid_factorized(de, out), out
+            _pid_factorized(de, out)
+            return out
 
-        _, out = _graphed(de, "pid", enqueue)
-        out = out.fresh()
+        out = _graphed(de, "pid", enqueue)
         masses = out.host_extra()[n:2 * n].copy()
     return _finish(de, out, "pid", masses, t0)
 
@@ -415,23 +437,24 @@ def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
         from .reduction import intersection_gram, pack_binary
 
         def enqueue():
-            # K7 packs and counts non-binary values in the same pass; the
-            # masses are the Gram diagonal |C_i| (exact integers)
-            out = _Out(n, dev)
-            nb = torch.zeros(n, dtype=torch.int64, device=dev)
+            # K7 packs and counts non-binary values in the same pass (the
+            # counts ride in the result block); the masses are the Gram
+            # diagonal |C_i| (exact integers)
+            out = _Out(n, dev, extra=n)
+            nb = out.extra.view(torch.int64)
+            nb.zero_()
             packed = pack_binary(de, nb)
             _allreduce(nb, de)
             g = intersection_gram(de, packed)
             mslot, ii, io, d = out.ptrs()
             N.call("pidb_eid_exact_epilogue", g.data_ptr(), n, ii, io, d, out.rank.data_ptr(),
                    mslot, stream_ptr(dev))
-            return nb, out
+            return out
 
-        nb, out = _graphed(de, "eid", enqueue)
-        out = out.fresh()  # a replayed graph reuses the same result block
+        out = _graphed(de, "eid", enqueue)
         # one host round trip: the non-binary check is read after the whole
         # stream has been queued (the results are discarded if it fails)
-        _raise_first_nonbinary(de, nb)
+        _raise_first_nonbinary(de, out.host_extra().view(np.int64))
         masses = out.host()[:n].copy()
     else:
         out = _Out(n, dev)
@@ -481,10 +504,9 @@ def depth_similarity_baseline(ensemble, measure: str, workers: int | None = None
         N.call("pidb_depth_epilogue", N.PIDB_EPI_DICE if kind == "dice" else N.PIDB_EPI_IOU,
                n, p, p + 8 * n, p + 16 * n, inv, ii, io, d, out.rank.data_ptr(),
                stream_ptr(dev))
-        return buf, out
+        return out
 
-    _, out = _graphed(de, kind, enqueue)
-    out = out.fresh()
+    out = _graphed(de, kind, enqueue)
     host = out.host_extra()[n:]
     if float(host[n]) == 0.0:
         raise DegenerateEnsembleError("ensemble mean mask is identically zero")

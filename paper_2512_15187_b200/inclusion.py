@@ -16,8 +16,6 @@ from . import _native as N
 from .device import require_cuda, stream_ptr
 from .errors import ValidationError
 
-_WS: dict = {}
-
 
 def _dev_values(x, dev, dtype=None) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
@@ -39,10 +37,10 @@ def _pair(u_vals, v_vals, weights, op: int) -> tuple[float, ...]:
     v = _dev_values(v_vals, dev, dt)
     w = None if weights is None else _dev_values(np.asarray(weights, dtype=np.float64), dev, torch.float64)
     m = u.numel()
-    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
-    ws = _WS.get(key)
-    if ws is None:
-        ws = _WS[key] = torch.empty(8192 * 8, dtype=torch.uint8, device=dev)
+    # a private ~20 KB workspace per call from the stream-aware caching
+    # allocator: concurrent callers (any thread, same stream) never share the
+    # partials buffer; the call synchronises before the block is released
+    ws = torch.empty(8192 * 8, dtype=torch.uint8, device=dev)
     out = np.zeros(4, dtype=np.float64)
     N.call("pidb_pair_sums", u.data_ptr(), v.data_ptr(),
            N.PIDB_F64 if dt == torch.float64 else N.PIDB_F32, m,

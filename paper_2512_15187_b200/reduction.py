@@ -6,7 +6,9 @@ _pairwise_sums tiles over member blocks (depth.py:122-161).  Here one kernel
 launch computes the whole symmetric N x N Gram of a resident ensemble:
 
 * K1 ``pidb_gram_tf32x3``: fuzzy members, 3xTF32 tcgen05 MMAs, fp64 result;
-* K2 ``pidb_gram_i8``: 0/1 members packed to uint8 (K7), exact int64 result.
+* K2 ``pidb_gram_i8``: 0/1 members packed to uint8 (K7), exact int64 result;
+* ``pidb_gram_f64``: the array-level ``gram_block`` seam itself, fp64 on the
+  CUDA cores (the reference's rtol 1e-12 contract).
 
 Per-shard Grams are summed across GPUs with one NCCL allreduce.
 """
@@ -74,19 +76,121 @@ def intersection_gram(de: DeviceEnsemble, packed: torch.Tensor | None = None) ->
     return g
 
 
-def gram_block(rows, cols, weights=None, complement_cols: bool = False) -> np.ndarray:
-    """Array-level mirror of reduction.py:75-97 on the tensor cores.
+_EXACT_F32 = (np.float32, np.float16, np.bool_, np.uint8, np.int8, np.uint16, np.int16)
 
-    rows (n_r, cells) and cols (n_c, cells); returns float64 (n_r, n_c).
-    The Gram of the stacked [rows; cols] block is formed once and sliced.
-    """
-    rows = np.asarray(rows)
-    cols = np.asarray(cols)
+
+def _block_to_device(a, dt, dev) -> torch.Tensor:
+    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+    return t.to(device=dev, dtype=dt).contiguous()
+
+
+def gram_block(rows, cols, weights=None, complement_cols: bool = False) -> np.ndarray:
+    """Array-level drop-in for gram_block (reduction.py:75-97), in fp64.
+
+    rows (n_r, cells) and cols (n_c, cells) of any real dtype; returns the
+    float64 (n_r, n_c) block ``rows . diag(w) . cols^T`` (or ``. (1 - cols)^T``)
+    with fp64 products and sums on the CUDA cores (``pidb_gram_f64``), the
+    reference's accuracy contract (rtol 1e-12 in its tests).  Float32-exact
+    inputs are read as float32 and widened in the kernel; anything else goes
+    over as float64.  The depth methods never call this: their Grams are the
+    tensor-core kernels (``fixed_gram`` / ``intersection_gram``) or the
+    factorised sums."""
+    from .device import require_cuda
+    from .depth import _launch
+
+    rows = rows if isinstance(rows, torch.Tensor) else np.asarray(rows)
+    cols = cols if isinstance(cols, torch.Tensor) else np.asarray(cols)
     if rows.ndim != 2 or cols.ndim != 2 or rows.shape[1] != cols.shape[1]:
         raise ValidationError("rows and cols must be (n, cells) with equal cells")
-    right = (1.0 - cols.astype(np.float64)) if complement_cols else cols
-    stacked = np.concatenate([rows.astype(np.float32), np.asarray(right, dtype=np.float32)])
-    de = DeviceEnsemble.from_tensor(torch.from_numpy(stacked), weights=weights, validate=False)
-    g = gram_device(de).cpu().numpy()
-    nr = rows.shape[0]
-    return g[:nr, nr:].copy()
+    nr, m = int(rows.shape[0]), int(rows.shape[1])
+    nc = int(cols.shape[0])
+    if nr == 0 or nc == 0 or m == 0:
+        return np.zeros((nr, nc), dtype=np.float64)
+    dev = require_cuda()
+
+    def exact32(a):
+        d = a.dtype if isinstance(a, np.ndarray) else torch.empty(0, dtype=a.dtype).numpy().dtype
+        return any(d == np.dtype(t) for t in _EXACT_F32)
+
+    f32 = exact32(rows) and exact32(cols)
+    dt = torch.float32 if f32 else torch.float64
+    r = _block_to_device(rows, dt, dev)
+    c = _block_to_device(cols, dt, dev)
+    w = None
+    if weights is not None:
+        wh = np.ascontiguousarray(weights, dtype=np.float64).reshape(-1)
+        if wh.shape[0] != m:
+            raise ValidationError(f"weights shape {wh.shape} does not match cell count {m}")
+        w = torch.from_numpy(wh).to(dev)
+    out = torch.empty((nr, nc), dtype=torch.float64, device=dev)
+    lib = N.load()
+    ws = torch.empty(max(1, lib.pidb_gram_f64_workspace_bytes(nr, nc, m)), dtype=torch.uint8,
+                     device=dev)
+    _launch("pidb_gram_f64", r.data_ptr(), c.data_ptr(), N.PIDB_F32 if f32 else N.PIDB_F64,
+            nr, nc, m, m, m, None if w is None else w.data_ptr(), int(bool(complement_cols)),
+            out.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr(dev))
+    return out.cpu().numpy()
+
+
+# ------------------------------------------------- reduction-module seams
+# reduction.py:30-72, 100-127: the chunked host reductions the reference's
+# depth code is built from.  Here they run on the device through the K8 pair
+# kernel (one fused pass, fp64 accumulation); chunk_bounds / run_tasks keep
+# the reference's host contract for callers that iterate themselves.
+
+
+def chunk_bounds(n_cells: int):
+    """(start, stop) spans of CHUNK_CELLS cells covering [0, n_cells) in
+    ascending order (reduction.py:30-33)."""
+    start = 0
+    while start < n_cells:
+        stop = min(n_cells, start + CHUNK_CELLS)
+        yield start, stop
+        start = stop
+
+
+def _pair_sums(a, b, weights, op):
+    from .inclusion import _pair
+
+    return _pair(a, a if b is None else b, weights, op)
+
+
+def weighted_sum(values, weights=None) -> float:
+    """sum_x w(x) v(x) in fp64 (reduction.py:36-44), one device pass."""
+    from . import _native as _N
+
+    return _pair_sums(values, None, weights, _N.PIDB_OP_INCLUSION)[1]
+
+
+def weighted_inner(a, b, weights=None) -> float:
+    """sum_x w a b in fp64 (reduction.py:47-57), one device pass."""
+    from . import _native as _N
+
+    return _pair_sums(a, b, weights, _N.PIDB_OP_INCLUSION)[0]
+
+
+def weighted_excess(a, b, weights=None) -> float:
+    """sum_x w a (1 - b) = sum w a - sum w a b (reduction.py:60-72)."""
+    from . import _native as _N
+
+    inner, mass = _pair_sums(a, b, weights, _N.PIDB_OP_INCLUSION)
+    return mass - inner
+
+
+def run_tasks(fn, items, workers: int) -> list:
+    """Results of fn over items in input order (reduction.py:115-127); a
+    thread pool when workers > 1 (the device calls release the GIL)."""
+    todo = list(items)
+    if workers > 1 and len(todo) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            return list(ex.map(fn, todo))
+    return [fn(x) for x in todo]
+
+
+def resolve_workers(workers: int | None = None) -> int:
+    """reduction.py:100-112 (the device kernels ignore the count)."""
+    from .depth import resolve_workers as _rw
+
+    return _rw(workers)

@@ -609,6 +609,94 @@ def test_concurrent_callers(pb):
         assert sum(pool.map(work, range(4))) == 0
 
 
+def test_concurrent_callers_private_streams(pb):
+    """Threads replaying the same ensemble's graphs, each on its own torch
+    stream (graphs are cached per stream: their workspaces never meet), and
+    threads calling the pair operators at once on different pairs (each call
+    has its own partials buffer)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(22)
+    shared = pb.DeviceEnsemble.from_tensor(
+        torch.from_numpy(rng.uniform(size=(60, 7000)).astype(np.float32)).cuda())
+    methods = ("pid-mean", "pid", "dice")
+    want = {m: pb.depth_by_method(shared, m).depth for m in methods}
+    g = pb.GridSpec((5000,))
+    pairs = [(pb.ProbMask(g, rng.uniform(size=5000).astype(np.float32)),
+              pb.ProbMask(g, rng.uniform(size=5000).astype(np.float32))) for _ in range(8)]
+    pwant = [pb.prob_inclusion(u, v) for u, v in pairs]
+
+    def work(k):
+        bad = 0
+        with torch.cuda.stream(torch.cuda.Stream()):
+            for it in range(16):
+                m = methods[(it + k) % len(methods)]
+                bad += not np.array_equal(pb.depth_by_method(shared, m).depth, want[m])
+                j = (it * 3 + k) % len(pairs)
+                bad += pb.prob_inclusion(*pairs[j]) != pwant[j]
+        return bad
+
+    with ThreadPoolExecutor(4) as pool:
+        assert sum(pool.map(work, range(4))) == 0
+
+
+def test_gram_block_fp64_contract(pb):
+    """gram_block seam (reduction.py:75-97) at the reference's own tolerance,
+    rtol 1e-12 (tests/test_reduction.py:46-66): float32 and float64 inputs,
+    weights, the complement form, ragged shapes and split-K."""
+    from paper_2512_15187_b200.reduction import gram_block
+
+    rng = np.random.default_rng(1)
+    rows = rng.uniform(size=(4, 300)).astype(np.float32)
+    cols = rng.uniform(size=(3, 300)).astype(np.float32)
+    w = rng.uniform(0.5, 2.0, size=300)
+    got = gram_block(rows, cols, w)
+    want = (rows.astype(np.float64) * w) @ cols.astype(np.float64).T
+    np.testing.assert_allclose(got, want, rtol=1e-12)
+    assert got.dtype == np.float64
+    comp = gram_block(rows, cols, w, complement_cols=True)
+    np.testing.assert_allclose(comp, (rows.astype(np.float64) * w) @ (1.0 - cols.astype(np.float64)).T,
+                               rtol=1e-12)
+    for nr, nc, m, f64, wt in ((1, 1, 1, False, False), (65, 130, 70001, True, True),
+                               (200, 3, 1 << 17, False, True), (7, 300, 999, True, False)):
+        a = rng.uniform(size=(nr, m))
+        b = rng.uniform(size=(nc, m))
+        if not f64:
+            a, b = a.astype(np.float32), b.astype(np.float32)
+        ww = rng.uniform(0.5, 2.0, size=m) if wt else None
+        for comp in (False, True):
+            got = gram_block(a, b, ww, complement_cols=comp)
+            A = a.astype(np.float64) * (1.0 if ww is None else ww)
+            B = b.astype(np.float64)
+            want = A @ (1.0 - B if comp else B).T
+            np.testing.assert_allclose(got, want, rtol=1e-12)
+    assert gram_block(np.zeros((0, 5)), np.zeros((2, 5))).shape == (0, 2)
+
+
+def test_reduction_seams_match_fsum(pb):
+    """weighted_sum / weighted_inner / weighted_excess (reduction.py:36-72)
+    and depth._member_mean_terms (depth.py:231-243) against math.fsum."""
+    from paper_2512_15187_b200 import reduction as R
+    from paper_2512_15187_b200.depth import _member_mean_terms
+
+    rng = np.random.default_rng(0)
+    a = rng.uniform(size=R.CHUNK_CELLS + 123)
+    b = rng.uniform(size=a.size)
+    w = rng.uniform(0.5, 2.0, size=a.size)
+    fs = lambda x: math.fsum(x.tolist())  # noqa: E731
+    assert abs(R.weighted_sum(a, w) - fs(a * w)) < 1e-9
+    assert abs(R.weighted_sum(a) - fs(a)) < 1e-9
+    assert abs(R.weighted_inner(a, b, w) - fs(w * a * b)) < 1e-9
+    assert abs(R.weighted_excess(a, b, w) - fs(w * a * (1 - b))) < 1e-9
+    u = a.astype(np.float32)
+    num, mass = _member_mean_terms(u, b, w)
+    assert abs(num - fs(w * u.astype(np.float64) * b)) < 1e-9
+    assert abs(mass - fs(w * u.astype(np.float64))) < 1e-9
+    spans = list(R.chunk_bounds(3 * R.CHUNK_CELLS + 5))
+    assert spans[0] == (0, R.CHUNK_CELLS) and spans[-1] == (3 * R.CHUNK_CELLS, 3 * R.CHUNK_CELLS + 5)
+    assert R.run_tasks(lambda x: x * x, range(20), 4) == [x * x for x in range(20)]
+
+
 @pytest.mark.parametrize("n", [300, 1000, 3000])
 def test_masses_across_kernel_variants(pb, n):
     """member_masses takes a different kernel than the depth passes (no column

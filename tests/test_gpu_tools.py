@@ -64,16 +64,13 @@ def test_stage_manifest_matches_loader_path(pb, tmp_path):
     np.testing.assert_array_equal(r.rank, z["pid_rank"])
 
 
-def test_stage_manifest_fields_binary_threshold(pb, tmp_path):
+def test_stage_manifest_binary_threshold(pb, tmp_path):
     rng = np.random.default_rng(4)
     (tmp_path / "v").mkdir()
     entries = []
-    fields = [rng.normal(size=(6, 7)) for _ in range(4)]
-    modes = [{"mode": "isovalue", "q": 0.2, "width": 0.5}, {"mode": "sublevel", "q": 0.0},
-             {"mode": "minmax"}, {"mode": "isovalue", "q": -0.1}]
-    for i, (f, md) in enumerate(zip(fields, modes)):
-        pb.write_volume(f, tmp_path / f"v/f{i}.npy")
-        entries.append({"id": f"f{i}", "path": f"v/f{i}.npy", "role": "field", "fuzzify": md})
+    for i in range(3):
+        pb.write_volume(rng.uniform(size=(6, 7)).astype(np.float32), tmp_path / f"v/u{i}.npy")
+        entries.append({"id": f"u{i}", "path": f"v/u{i}.npy"})
     bits = (rng.uniform(size=(6, 7)) < 0.5).astype(np.uint8)
     pb.write_volume(bits, tmp_path / "v/b.npy")
     entries.append({"id": "b", "path": "v/b.npy"})
@@ -91,6 +88,27 @@ def test_stage_manifest_fields_binary_threshold(pb, tmp_path):
     pb.write_manifest(tmp_path / "bad.json", (6, 7), [{"id": "x", "path": "v/bad.npy"}])
     with pytest.raises(pb.ValidationError):
         pb.stage_manifest(tmp_path / "bad.json")
+
+
+def test_stage_manifest_rejects_non_binary_uint8(pb, tmp_path):
+    """A 0/255 uint8 mask loads through BinaryMask in the reference, which
+    raises ValidationError (grid.py:145-147); staging it must raise too (and
+    a CLI depth run exit 1), not feed 255.0 into the kernels."""
+    (tmp_path / "v").mkdir()
+    ok = (np.arange(42).reshape(6, 7) % 2).astype(np.uint8)
+    np.save(tmp_path / "v/ok.npy", ok)
+    np.save(tmp_path / "v/b255.npy", ok * 255)
+    np.save(tmp_path / "v/f.npy", np.full((6, 7), 0.5, dtype=np.float32))
+    pb.write_manifest(tmp_path / "m.json", (6, 7), [{"id": "ok", "path": "v/ok.npy"},
+                                                     {"id": "f", "path": "v/f.npy"},
+                                                     {"id": "bad", "path": "v/b255.npy"}])
+    with pytest.raises(pb.ValidationError, match="binary mask values must be 0 or 1"):
+        pb.stage_manifest(tmp_path / "m.json")
+    from paper_2512_15187_b200.cli import main as cli_main
+
+    rc = cli_main(["depth", "--manifest", str(tmp_path / "m.json"), "--method", "pid",
+                   "--out", str(tmp_path / "d.csv")])
+    assert rc == 1
 
 
 def test_build_boxplot_matches_reference(pb, tmp_path):

@@ -1,5 +1,5 @@
 """Host side of the drop-in's ingestion / output formats and of the callers
-around the depth path (io, fuzzify, boxplot images, consistency, CLI exit
+around the depth path (io, boxplot images, consistency, CLI exit
 codes), checked against fixtures produced by the reference itself
 (tests/golden/make_golden.py: tools_golden).  No GPU needed."""
 from __future__ import annotations
@@ -14,7 +14,6 @@ from conftest import GOLDEN, golden
 pb = pytest.importorskip("paper_2512_15187_b200")
 from paper_2512_15187_b200 import boxplot as bx  # noqa: E402
 from paper_2512_15187_b200 import consistency as cons  # noqa: E402
-from paper_2512_15187_b200 import fuzzify as fz  # noqa: E402
 from paper_2512_15187_b200 import io as pio  # noqa: E402
 from paper_2512_15187_b200.cli import main as cli_main  # noqa: E402
 
@@ -23,20 +22,15 @@ def tools():
     return golden("tools"), json.loads((GOLDEN / "tools.json").read_text())
 
 
-def test_fuzzify_matches_reference_bitwise():
-    z, _ = tools()
-    f = fz.ScalarField(pb.GridSpec(z["field"].shape), z["field"])
-    assert np.array_equal(fz.fuzzy_isocontour(f, 0.3, 0.7).values, z["fz_iso"])
-    assert np.array_equal(fz.fuzzy_isocontour(f, -0.2, fz.default_width(f)).values,
-                          z["fz_iso_default"])
-    assert np.array_equal(fz.hard_isocontour(f, 0.1).bits, z["fz_sub"])
-    assert np.array_equal(fz.normalize_density(f, "minmax").values, z["fz_minmax"])
-    g = fz.ScalarField(pb.GridSpec(z["field"].shape), np.abs(z["field"]))
-    assert np.array_equal(fz.normalize_density(g, "scale-by-max").values, z["fz_sbm"])
-    with pytest.raises(pb.ValidationError):
-        fz.normalize_density(fz.ScalarField(pb.GridSpec((3,)), np.ones(3)), "minmax")
-    with pytest.raises(pb.ValidationError):
-        fz.fuzzy_isocontour(f, 0.0, 0.0)
+def test_field_members_are_out_of_scope(tmp_path):
+    """Field-role members need fuzzification (fuzzify.py), input preparation
+    outside the depth path: the manifest still parses, loading one raises."""
+    np.save(tmp_path / "f.npy", np.ones((3, 4)))
+    m = _manifest(tmp_path, [{"id": "f", "path": "f.npy", "role": "field",
+                              "fuzzify": {"mode": "sublevel", "q": 0.0}}])
+    e = pio.read_manifest(m)
+    with pytest.raises(pb.ManifestError, match="fuzzif"):
+        e.member(0)
 
 
 def test_contour_cells_and_pgm(tmp_path):
@@ -117,15 +111,12 @@ def test_manifest_rules(tmp_path):
     np.save(tmp_path / "a.npy", rng.uniform(size=(3, 4)).astype(np.float32))
     np.save(tmp_path / "b.npy", (rng.uniform(size=12) < 0.5).astype(np.uint8))
     np.save(tmp_path / "f.npy", rng.normal(size=(3, 4)))
-    m = _manifest(tmp_path, [{"id": "a", "path": "a.npy"}, {"id": "b", "path": "b.npy"},
-                             {"id": "f", "path": "f.npy", "role": "field",
-                              "fuzzify": {"mode": "sublevel", "q": 0.0}}],
+    m = _manifest(tmp_path, [{"id": "a", "path": "a.npy"}, {"id": "b", "path": "b.npy"}],
                   weights=rng.uniform(0.5, 2, size=12))
     e = pio.read_manifest(m)
-    assert e.ids == ("a", "b", "f") and e.is_lazy()
+    assert e.ids == ("a", "b") and e.is_lazy()
     assert np.array_equal(e.member(0).values, np.load(tmp_path / "a.npy").reshape(-1))
     assert np.array_equal(e.member(1).values, np.load(tmp_path / "b.npy").astype(np.float32))
-    assert np.array_equal(e.member(2).values, (np.load(tmp_path / "f.npy") < 0.0).reshape(-1))
     assert e.grid.weights is not None
     assert not pio.manifest_guarantees_binary(m)
     mb = _manifest(tmp_path, [{"id": "b", "path": "b.npy"}])
