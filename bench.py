@@ -530,18 +530,29 @@ def run_pid_secondary(args, rank, world, pg, dev, pk):
                              "frac": ach / pk["hbm_gbs"], "kernels_ms": [k1, k2],
                              "algorithmic_bytes": 2 * b, "note": "exact fp64, two HBM passes"}
         else:
-            kg, _ = kernel_ms(ev, "pidb_gram_tf32x3_sums")
+            kg, _ = kernel_ms(ev, "pidb_gram_fixed_sums")
+            kp, _ = kernel_ms(ev, "pidb_fixed_pack")
             flops = n * (n + 1) * de.m  # symmetric Gram, 2 flops per MAC
             ach = flops / (kg * 1e-3) / 1e12
-            o["roofline"] = {"bound": "tensor", "achieved": ach, "unit": "TFLOP/s",
-                             "peak": TF32_TFLOPS_PROBE / 3,
-                             "frac": ach / (TF32_TFLOPS_PROBE / 3), "kernel_ms": kg,
-                             "algorithmic_flops": flops,
-                             "peak_src": "cuBLAS TF32 probe / 3 (3xTF32 = 3 MMA passes)"}
+            nib = (n + 127) // 128
+            executed = nib * (nib + 1) // 2 * ((de.m + 31) // 32) * 10 * 2 * 128 * 128 * 32
+            mode_peak = INT8_TOPS_PROBE / 10  # 10 digit-pair int8 MMAs per product
+            o["roofline"] = {"bound": "tensor",
+                             "kernel": "gram_fx_kernel (K1x: fixed-point digits, tcgen05 kind::i8, "
+                                       "exact int32 accumulation, fused PID sums)",
+                             "achieved": ach, "unit": "TFLOP/s", "peak": mode_peak,
+                             "frac": ach / mode_peak,
+                             "peak_src": "cuBLAS INT8 probe / 10 (10 digit-pair MMAs per product)",
+                             "frac_vs_tf32x3": ach / (TF32_TFLOPS_PROBE / 3),
+                             "executed_int8_ops": executed,
+                             "executed_frac_of_int8_peak": executed / (kg * 1e-3) / 1e12 / INT8_TOPS_PROBE,
+                             "kernel_ms": kg, "pack_ms": kp, "algorithmic_flops": flops}
+            o["certifier"] = dict(D.LAST_GRAM_CERT)
         out[alg] = o
     if len(results) == 2:
         a, b = results["gram"], results["factorized"]
         out["gram_vs_exact"] = {
+            "max_abs_depth_err": float(np.abs(a.depth - b.depth).max()),
             "max_rel_depth_err": float(np.abs(a.depth - b.depth).max() / np.abs(b.depth).max()),
             "rank_mismatches": int(np.sum(a.rank != b.rank)),
             "min_depth_gap": float(np.min(np.diff(np.sort(b.depth))))}

@@ -123,24 +123,37 @@ size_t pidb_gram_i8_workspace_bytes(int64_t n, int64_t m);
 int pidb_gram_i8(const uint8_t* b, int64_t n, int64_t m, int64_t ldb,
                  int64_t* gram, void* ws, size_t ws_bytes, void* stream);
 
-/* ---------------------------------------------------------------- K1 ----
- * Weighted Gram G[i*n+j] = sum_x w(x) u_i(x) u_j(x) in fp64 from 3xTF32
- * tcgen05 MMAs (hi/lo split, fp32 TMEM accumulators flushed to fp64 every
- * <=512 cells).  Replaces gram_block (reduction.py:75-97) as used by
- * depth_pid/_pairwise_sums (depth.py:122-161, 213-228).  Float32 members only. */
-size_t pidb_gram_tf32x3_workspace_bytes(int64_t n, int64_t m);
-int pidb_gram_tf32x3(const float* u, int64_t n, int64_t m, int64_t ld,
-                     const double* w, double* gram, void* ws, size_t ws_bytes,
-                     void* stream);
-
-/* K1 with the PID sums fused into its epilogue (no N x N Gram in HBM):
- *   row_plain[i] = sum_j G[i,j],  col_inv[i] = sum_j inv_j G[i,j]
- * (depth.py:156-160 with G symmetric), inv = inverse masses (n, device).
- * Same workspace as pidb_gram_tf32x3; outputs are additive over cell
- * shards. */
-int pidb_gram_tf32x3_sums(const float* u, int64_t n, int64_t m, int64_t ld,
-                          const double* w, const double* inv, double* row_plain,
-                          double* col_inv, void* ws, size_t ws_bytes, void* stream);
+/* --------------------------------------------------------------- K1x ----
+ * Fixed-point Gram on the int8 tensor cores with exact integer accumulation
+ * (the tensor-core formulation of _pairwise_sums/gram_block for PID,
+ * depth.py:122-161 / reduction.py:75-97; DESIGN.md §3 K1).
+ *
+ * pidb_fixed_pack: a = u * sqrt(w / wmax) (w nullable: a = u), values in
+ * [0, 1]; q = rint(a 2^31) as four base-256 digits, stored per 32-cell block
+ * as one 128-byte line [d0 x32 | d1 x32 | d2 x32 | d3 x32]; ldq >=
+ * pidb_fixed_ld(m) bytes, a multiple of 128, q 128-byte aligned.
+ * soft_count[i] (nullable, zero-filled by the caller) += cells of member i
+ * whose q has non-zero low 24 bits (the only cells with a truncation tail;
+ * used by the rank certifier's error bound). */
+int64_t pidb_fixed_ld(int64_t m);
+int pidb_fixed_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                    const double* w, double wmax, uint8_t* q, int64_t ldq,
+                    uint64_t* soft_count, void* stream);
+/* G[i*n+j] = wmax * 2^-62 * sum_x (digit-pair levels 0..3 of q_i q_j): every
+ * product accumulates exactly (int32 TMEM, folded into fp64 every 8192
+ * cells); |G - G_exact| <= wmax (2^-32 (A_i + A_j) + m 2^-64 +
+ * 2.78e-9 min(soft_i, soft_j)), A = sum_x a (DESIGN.md §3 K1).
+ * `sums` selects the workspace of pidb_gram_fixed_sums (1) or of the full
+ * Gram (0). */
+size_t pidb_gram_fixed_workspace_bytes(int64_t n, int64_t m, int sums);
+int pidb_gram_fixed(const uint8_t* q, int64_t n, int64_t m, int64_t ldq, double wmax,
+                    double* gram, void* ws, size_t ws_bytes, void* stream);
+/* The PID sums of the same Gram fused into the tile epilogue (no n x n
+ * matrix in HBM): row_plain[i] = sum_j G[i,j], col_inv[i] = sum_j inv_j
+ * G[i,j] (depth.py:155-160, G symmetric); additive over cell shards. */
+int pidb_gram_fixed_sums(const uint8_t* q, int64_t n, int64_t m, int64_t ldq, double wmax,
+                         const double* inv, double* row_plain, double* col_inv, void* ws,
+                         size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------ K1-f64 ----
  * gram_block seam (reduction.py:75-97) in fp64 on the CUDA cores:

@@ -1,0 +1,456 @@
+// K1: the fuzzy Gram G = U diag(w) U^T on the int8 tensor cores with EXACT
+// integer accumulation (fixed-point digit slices, "Ozaki" style).
+//
+// Replaces the fp64 BLAS tile products of the exact PID:
+//   depth_pid / _pairwise_sums  /root/reference/pkg/src/fuzzdepth/depth.py:122-161, 213-228
+//   gram_block                  /root/reference/pkg/src/fuzzdepth/reduction.py:75-97
+//
+// Why not TF32: the tensor core accumulates fp32 with truncation, which
+// biases every 3xTF32 Gram entry by ~1e-6 relative -- 14x the smallest
+// depth gap at BASELINE configs[3].  Integer MMAs accumulate exactly.
+//
+// Representation (pidb_fixed_pack, one HBM pass): every member value u in
+// [0, 1] (times sqrt(w / w_max) on weighted grids, so that G = w_max * sum
+// a_i a_j) becomes q = rint(a * 2^31) <= 2^31, split into four base-256
+// digits d0 (0..128), d1, d2, d3.  Per 32-cell block a member row stores the
+// digits plane by plane: [d0 x32 | d1 x32 | d2 x32 | d3 x32] = one 128-byte
+// line, so a TMA box of 128 rows x 128 bytes with SWIZZLE_128B is directly
+// the K-major operand of tcgen05.mma.kind::i8 (K = 32) and digit plane k of
+// it is the same descriptor advanced by 32 bytes.
+//
+// Products: q_i q_j = 2^24 * sum_s 2^(8(3-s)) L_s with L_s = sum_{k+l=s}
+// d_k e_l; the levels s = 0..3 (10 digit pairs) are kept, the dropped
+// levels 4..6 are < 2.8e-9 per cell product and zero whenever either value
+// has no low-order digits (0, 1 and every value that quantises to a
+// multiple of 2^-7).  Each level accumulates in its own int32 TMEM
+// accumulator (M = N = 128, 4 x 128 = all 512 columns) -- exact for 256
+// stages (8192 cells; worst case 1.6e9 < 2^31) -- then the epilogue warps
+// fold v = ((L0*256 + L1)*256 + L2)*256 + L3 (an integer < 2^53, exact in fp64) into fp64
+// accumulators held in registers.  Emulated against the fp64 Gram
+// (tools/fixed_gram_emulation.py): depth error <= 3.2e-9 at N = 300 with
+// uniform, u^8 and ellipsoid members, 0 rank swaps.
+//
+// Work: 128 x 128 tiles of the upper block triangle x split-K (one wave);
+// diagonal tiles load one operand.  Warps (576 threads): 0 TMA producer
+// (6-stage ring, 32 KB per stage), 1 MMA issuer, 2-17 epilogue (TMEM lane
+// quadrant = warp % 4, 32 columns each).  Outputs per (tile, split) unit:
+// the fp64 tile, or (PID) its row sums, inverse-mass-weighted row sums and
+// the two column counterparts; fixed-order reductions finish both.
+#include <algorithm>
+#include <cmath>
+
+#include "tcgen05.cuh"
+
+namespace pidb {
+namespace {
+
+constexpr int kB = 128;                      // tile edge (members)
+constexpr int kLine = 128;                   // bytes per member per stage (32 cells x 4 digits)
+constexpr int kCellsPerStage = 32;
+constexpr int kStages = 6;                   // 192 KB ring (also holds the 132 KB fp64 tile at the end)
+constexpr int kTileBytes = kB * kLine;       // 16 KB
+constexpr int kStageBytes = 2 * kTileBytes;  // A and B
+constexpr int kFlush = 256;                  // stages per int32 accumulation window
+constexpr int kEpiWarps = 16;
+constexpr int kThreads = (2 + kEpiWarps) * 32;
+constexpr uint32_t kIdesc = tc::idesc(tc::kCS32, tc::kU8, kB, kB);
+constexpr double kTwoPow31 = 2147483648.0;
+
+struct FxParams {
+  int n, nib, ntiles, splits, kblocks, kb_per;
+  int sums;           // 1: tile sums (PID), 0: fp64 tiles
+  const double* inv;  // sums: inverse masses (n)
+  double* part;       // sums: [units][4][kB]; tiles: [units][kB][kB]
+};
+
+__host__ __device__ __forceinline__ void fx_tile(int t, int& ib, int& jb) {
+  int j = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while (j * (j + 1) / 2 > t) --j;
+  while ((j + 1) * (j + 2) / 2 <= t) ++j;
+  jb = j;
+  ib = t - j * (j + 1) / 2;
+}
+
+// ---------------------------------------------------------------- packing
+// One warp per (member row, segment of 64 blocks of 32 cells); lane = cell.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    fx_pack_kernel(const T* __restrict__ u, int64_t ld, int n, int64_t m,
+                   const double* __restrict__ w, double inv_wmax, uint8_t* __restrict__ q,
+                   int64_t ldq, int64_t nblk, int64_t nseg, unsigned long long* __restrict__ soft) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int k = lane >> 3, wi = lane & 7;
+  for (int64_t unit = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       unit < (int64_t)n * nseg; unit += warps) {
+    const int64_t row = unit / nseg, seg = unit - row * nseg;
+    const int64_t b0 = seg * 64, b1 = min(nblk, b0 + 64);
+    const T* src = u + row * ld;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(q + row * ldq);
+    unsigned int cnt = 0;
+#pragma unroll 4
+    for (int64_t b = b0; b < b1; ++b) {
+      const int64_t x = b * kCellsPerStage + lane;
+      double a = 0.0;
+      if (x < m) {
+        a = (double)src[x];
+        if (w) a *= sqrt(w[x] * inv_wmax);
+      }
+      uint32_t qq = (uint32_t)__double2uint_rn(a * kTwoPow31);
+      qq = min(qq, 0x80000000u);
+      // byte k of `packed` = digit k (most significant first)
+      const uint32_t packed = (qq >> 24) | (((qq >> 16) & 255u) << 8) | (((qq >> 8) & 255u) << 16) |
+                              ((qq & 255u) << 24);
+      cnt += __popc(__ballot_sync(0xffffffffu, (qq & 0xFFFFFFu) != 0u));
+      // lane L writes word L of the 128-byte line: plane k = L / 8, cells
+      // 4 (L % 8) .. +3 -> digit k of lanes 4 wi .. 4 wi + 3
+      uint32_t word = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t s = __shfl_sync(0xffffffffu, packed, 4 * wi + t);
+        word |= ((s >> (8 * k)) & 255u) << (8 * t);
+      }
+      dst[b * (kLine / 4) + lane] = word;
+    }
+    if (soft && lane == 0 && cnt) atomicAdd(soft + row, (unsigned long long)cnt);
+  }
+}
+
+// ------------------------------------------------------------------- Gram
+__device__ __forceinline__ void epi_sync() {  // the 16 epilogue warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gram_fx_kernel(const __grid_constant__ CUtensorMap tmap, const FxParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  unsigned char* ring = smem_raw + pad;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int unit = blockIdx.x;
+  const int t = unit % p.ntiles, split = unit / p.ntiles;  // split-major: one K window at a time
+  int ib, jb;
+  fx_tile(t, ib, jb);
+  const bool diag = ib == jb;
+  const int kb0 = split * p.kb_per;
+  const int nk = max(0, min(p.kblocks, kb0 + p.kb_per) - kb0);
+  const int nflush = (nk + kFlush - 1) / kFlush;
+
+  if (threadIdx.x == 0) {
+    prefetch_tma_desc(&tmap);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, kEpiWarps);
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      const uint64_t pol = policy_evict_last();  // panels are re-read by the other tiles
+      const uint32_t bytes = diag ? kTileBytes : kStageBytes;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int k = 0; k < nk; ++k) {
+        mbar_wait(&empty[s], ph ^ 1u);
+        unsigned char* a = ring + s * kStageBytes;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        const int x = (kb0 + k) * kLine;
+        tma_load_2d(a, &tmap, x, ib * kB, &full[s], pol);
+        if (!diag) tma_load_2d(a + kTileBytes, &tmap, x, jb * kB, &full[s], pol);
+        if (++s == kStages) { s = 0; ph ^= 1u; }
+      }
+    }
+  } else if (warp == 1) {
+    if (tc::elect_one()) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int k = 0; k < nk; ++k) {
+        const int kw = k % kFlush;
+        if (kw == 0 && k > 0) {
+          mbar_wait(tempty, (uint32_t)((k / kFlush - 1) & 1));  // epilogue drained TMEM
+          tc::fence_after();
+        }
+        mbar_wait(&full[s], ph);
+        tc::fence_after();
+        const uint32_t a = smem_u32(ring + s * kStageBytes);
+        const uint64_t da = tc::desc_kmajor_sw128(a);
+        const uint64_t db = diag ? da : tc::desc_kmajor_sw128(a + kTileBytes);
+        const uint32_t acc = kw != 0;
+        // level s = k + l accumulates at TMEM column 128 s; digit plane k is
+        // the descriptor advanced by 32 bytes (2 x 16-byte units) per plane
+#pragma unroll
+        for (int lv = 0; lv < 4; ++lv)
+#pragma unroll
+          for (int dk = 0; dk <= lv; ++dk)
+            tc::mma_i8(tmem + 128u * lv, da + 2 * dk, db + 2 * (lv - dk), kIdesc,
+                       dk != 0 ? 1u : acc);
+        tc::commit(&empty[s]);
+        if (kw == kFlush - 1 || k == nk - 1) tc::commit(tfull);
+        if (++s == kStages) { s = 0; ph ^= 1u; }
+      }
+    }
+  } else {
+    // epilogue: TMEM lane quadrant q (hardware rule: warp % 4), columns c0..c0+31
+    const int q = warp & 3, cc = (warp - 2) >> 2;
+    const int row = q * 32 + lane, c0 = cc * 32;
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+    double acc[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) acc[e] = 0.0;
+    for (int f = 0; f < nflush; ++f) {
+      mbar_wait(tfull, (uint32_t)(f & 1));
+      tc::fence_after();
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        // v = ((L0 * 256 + L1) * 256 + L2) * 256 + L3: integers < 2^53, exact in fp64
+        double v[4];
+#pragma unroll
+        for (int lv = 0; lv < 4; ++lv) {
+          uint32_t r[4];
+          tc::tmem_ld4(tbase + 128u * lv + 4u * h, r);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            v[e] = lv == 0 ? (double)(int32_t)r[e] : fma(v[e], 256.0, (double)(int32_t)r[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[4 * h + e] += v[e];
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+    }
+
+    // All stages are consumed: stage the fp64 tile in the free ring (row
+    // stride kB + 1 doubles), then sum / store it in a fixed order.
+    double* tile = reinterpret_cast<double*>(ring);
+    constexpr int kLd = kB + 1;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) tile[row * kLd + c0 + e] = acc[e];
+    epi_sync();
+    const int et = threadIdx.x - 64;  // 0..511
+    if (!p.sums) {
+      double* dst = p.part + (size_t)unit * kB * kB;
+      for (int e = et; e < kB * kB; e += kEpiWarps * 32) dst[e] = tile[(e / kB) * kLd + (e % kB)];
+    } else {
+      // et / 128 = 0: row sums, 1: rows weighted by inv_j, 2: column sums,
+      // 3: columns weighted by inv_i (off-diagonal tiles only)
+      const int kind = et >> 7, r = et & (kB - 1);
+      double s2 = 0.0;
+      if (kind == 0) {
+        for (int c = 0; c < kB; ++c) s2 += tile[r * kLd + c];
+      } else if (kind == 1) {
+        for (int c = 0; c < kB; ++c) {
+          const int gj = jb * kB + c;
+          s2 += (gj < p.n ? __ldg(p.inv + gj) : 0.0) * tile[r * kLd + c];
+        }
+      } else if (!diag) {
+        for (int x = 0; x < kB; ++x) {
+          const int gi = ib * kB + x;
+          const double wgt = kind == 2 ? 1.0 : (gi < p.n ? __ldg(p.inv + gi) : 0.0);
+          s2 += wgt * tile[x * kLd + r];
+        }
+      }
+      p.part[(size_t)unit * 4 * kB + et] = s2;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+// PID sums: row_plain[i] = sum_j G[i,j], col_inv[i] = sum_j inv_j G[i,j]
+// (G symmetric), over the tiles holding member i as a row (ib, jb >= ib) or
+// as a column (a < ib, ib), splits inner, in that fixed order.
+__global__ void fx_sums_reduce_kernel(const double* __restrict__ part, int n, int nib, int ntiles,
+                                      int splits, double scale, double* __restrict__ row_plain,
+                                      double* __restrict__ col_inv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int ib = i / kB, r = i - ib * kB;
+  double a = 0.0, b = 0.0;
+  for (int jb = ib; jb < nib; ++jb) {
+    const int t = jb * (jb + 1) / 2 + ib;
+    for (int s = 0; s < splits; ++s) {
+      const double* u = part + ((size_t)s * ntiles + t) * 4 * kB;
+      a += u[r];
+      b += u[kB + r];
+    }
+  }
+  for (int x = 0; x < ib; ++x) {
+    const int t = ib * (ib + 1) / 2 + x;
+    for (int s = 0; s < splits; ++s) {
+      const double* u = part + ((size_t)s * ntiles + t) * 4 * kB;
+      a += u[2 * kB + r];
+      b += u[3 * kB + r];
+    }
+  }
+  row_plain[i] = a * scale;
+  col_inv[i] = b * scale;
+}
+
+// G[i][j] = G[j][i] = scale * sum over splits of the tile holding (i, j), i <= j.
+__global__ void fx_tiles_reduce_kernel(const double* __restrict__ part, int n, int ntiles,
+                                       int splits, double scale, double* __restrict__ out) {
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
+    if (i > j) continue;
+    const int ib = i / kB, jb = j / kB;
+    const int t = jb * (jb + 1) / 2 + ib;
+    const double* src = part + ((size_t)t * kB + (i - ib * kB)) * kB + (j - jb * kB);
+    double acc = 0.0;
+    for (int s = 0; s < splits; ++s) acc += src[(size_t)s * ntiles * kB * kB];
+    acc *= scale;
+    out[e] = acc;
+    if (i != j) out[(int64_t)j * n + i] = acc;
+  }
+}
+
+struct FxPlan {
+  int nib, ntiles, splits, kblocks, kb_per, units;
+  size_t smem, ws_tiles, ws_sums;
+};
+
+FxPlan plan_fx(int64_t n, int64_t m) {
+  FxPlan g{};
+  g.nib = (int)((n + kB - 1) / kB);
+  g.ntiles = g.nib * (g.nib + 1) / 2;
+  g.kblocks = (int)((m + kCellsPerStage - 1) / kCellsPerStage);
+  const int sms = sm_count();
+  g.splits = std::max(1, std::min(g.kblocks, sms / g.ntiles));  // one wave when it fits
+  g.kb_per = (g.kblocks + g.splits - 1) / g.splits;
+  g.splits = (g.kblocks + g.kb_per - 1) / g.kb_per;               // every split non-empty
+  g.units = g.ntiles * g.splits;
+  g.smem = 1024 + (size_t)kStages * kStageBytes + 256;
+  // the first 256 bytes of a shared workspace hold other kernels' completion
+  // counters (zero between launches): partials start after them
+  g.ws_tiles = 256 + (size_t)g.units * kB * kB * sizeof(double);
+  g.ws_sums = 256 + (size_t)g.units * 4 * kB * sizeof(double);
+  return g;
+}
+
+int launch_gram_fx(const uint8_t* qd, int64_t n, int64_t m, int64_t ldq, const FxPlan& g,
+                   FxParams prm, cudaStream_t st) {
+  CUtensorMap tm;
+  int rc = encode_tma_2d(&tm, qd, CU_TENSOR_MAP_DATA_TYPE_UINT8, (uint64_t)ldq, (uint64_t)n,
+                         (uint64_t)ldq, kLine, kB, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc != PIDB_OK) return rc;
+  prm.n = (int)n; prm.nib = g.nib; prm.ntiles = g.ntiles; prm.splits = g.splits;
+  prm.kblocks = g.kblocks; prm.kb_per = g.kb_per;
+  PIDB_CUDA(cudaFuncSetAttribute(gram_fx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)g.smem));
+  gram_fx_kernel<<<g.units, kThreads, g.smem, st>>>(tm, prm);
+  PIDB_LAUNCH_CHECK("gram_fx_kernel");
+  return PIDB_OK;
+}
+
+}  // namespace
+}  // namespace pidb
+
+using namespace pidb;
+
+extern "C" int64_t pidb_fixed_ld(int64_t m) {
+  return m < 1 ? 0 : (m + kCellsPerStage - 1) / kCellsPerStage * kLine;
+}
+
+extern "C" int pidb_fixed_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                               const double* w, double wmax, uint8_t* q, int64_t ldq,
+                               uint64_t* soft_count, void* stream) {
+  PIDB_REQUIRE(u && q && n >= 1 && m >= 1 && ld >= m, "bad arguments to pidb_fixed_pack");
+  PIDB_REQUIRE(dtype == PIDB_F32 || dtype == PIDB_F64, "unknown dtype %d", dtype);
+  PIDB_REQUIRE(ldq >= pidb_fixed_ld(m) && ldq % kLine == 0 &&
+                   (reinterpret_cast<uintptr_t>(q) & 127) == 0,
+               "digit rows need ldq >= pidb_fixed_ld(m), a multiple of 128, 128-byte aligned");
+  PIDB_REQUIRE(!w || wmax > 0.0, "weighted packing needs wmax > 0");
+  const int64_t nblk = (m + kCellsPerStage - 1) / kCellsPerStage;
+  const int64_t nseg = (nblk + 63) / 64;
+  const int64_t warps = n * nseg;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 16));
+  cudaStream_t st = (cudaStream_t)stream;
+  const double iw = w ? 1.0 / wmax : 1.0;
+  if (dtype == PIDB_F32)
+    fx_pack_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(u), ld, (int)n, m, w,
+                                                  iw, q, ldq, nblk, nseg,
+                                                  reinterpret_cast<unsigned long long*>(soft_count));
+  else
+    fx_pack_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(u), ld, (int)n, m, w,
+                                                   iw, q, ldq, nblk, nseg,
+                                                   reinterpret_cast<unsigned long long*>(soft_count));
+  PIDB_LAUNCH_CHECK("fx_pack_kernel");
+  return PIDB_OK;
+}
+
+extern "C" size_t pidb_gram_fixed_workspace_bytes(int64_t n, int64_t m, int sums) {
+  if (n < 1 || m < 1) return 0;
+  const FxPlan g = plan_fx(n, m);
+  return sums ? g.ws_sums : g.ws_tiles;
+}
+
+static int fx_check(const uint8_t* q, int64_t n, int64_t m, int64_t ldq) {
+  PIDB_REQUIRE(q && n >= 1 && m >= 1, "bad arguments to the fixed-point Gram");
+  PIDB_REQUIRE(ldq >= pidb_fixed_ld(m) && ldq % kLine == 0 &&
+                   (reinterpret_cast<uintptr_t>(q) & 127) == 0,
+               "digit rows need ldq >= pidb_fixed_ld(m), a multiple of 128, 128-byte aligned");
+  PIDB_REQUIRE(n <= (1 << 20), "too many members for the Gram");
+  PIDB_REQUIRE(m < ((int64_t)1 << 40), "too many cells");
+  return PIDB_OK;
+}
+
+extern "C" int pidb_gram_fixed(const uint8_t* q, int64_t n, int64_t m, int64_t ldq, double wmax,
+                               double* gram, void* ws, size_t ws_bytes, void* stream) {
+  int rc = fx_check(q, n, m, ldq);
+  if (rc != PIDB_OK) return rc;
+  PIDB_REQUIRE(gram, "null output");
+  const FxPlan g = plan_fx(n, m);
+  PIDB_REQUIRE(ws && ws_bytes >= g.ws_tiles, "workspace too small: need %zu bytes", g.ws_tiles);
+  FxParams prm{};
+  prm.sums = 0;
+  prm.part = reinterpret_cast<double*>(static_cast<char*>(ws) + 256);
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = launch_gram_fx(q, n, m, ldq, g, prm, st);
+  if (rc != PIDB_OK) return rc;
+  const double scale = wmax * std::ldexp(1.0, -38);
+  const int64_t total = n * n;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
+  fx_tiles_reduce_kernel<<<blocks, 256, 0, st>>>(prm.part, (int)n, g.ntiles, g.splits, scale, gram);
+  PIDB_LAUNCH_CHECK("fx_tiles_reduce_kernel");
+  return PIDB_OK;
+}
+
+extern "C" int pidb_gram_fixed_sums(const uint8_t* q, int64_t n, int64_t m, int64_t ldq,
+                                    double wmax, const double* inv, double* row_plain,
+                                    double* col_inv, void* ws, size_t ws_bytes, void* stream) {
+  int rc = fx_check(q, n, m, ldq);
+  if (rc != PIDB_OK) return rc;
+  PIDB_REQUIRE(inv && row_plain && col_inv, "null inverse masses or outputs");
+  const FxPlan g = plan_fx(n, m);
+  PIDB_REQUIRE(ws && ws_bytes >= g.ws_sums, "workspace too small: need %zu bytes", g.ws_sums);
+  FxParams prm{};
+  prm.sums = 1;
+  prm.inv = inv;
+  prm.part = reinterpret_cast<double*>(static_cast<char*>(ws) + 256);
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = launch_gram_fx(q, n, m, ldq, g, prm, st);
+  if (rc != PIDB_OK) return rc;
+  const double scale = wmax * std::ldexp(1.0, -38);
+  fx_sums_reduce_kernel<<<(int)((n + 127) / 128), 128, 0, st>>>(prm.part, (int)n, g.nib, g.ntiles,
+                                                               g.splits, scale, row_plain, col_inv);
+  PIDB_LAUNCH_CHECK("fx_sums_reduce_kernel");
+  return PIDB_OK;
+}

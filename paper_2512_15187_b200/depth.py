@@ -4,7 +4,7 @@ Same names, signatures, results and errors as the reference module
 /root/reference/pkg/src/fuzzdepth/depth.py; the arithmetic runs in libpidb:
 
   depth_pid_mean  (depth.py:246-287) -> K5 single HBM pass + K4 epilogue
-  depth_pid       (depth.py:213-228) -> K1 3xTF32 tcgen05 Gram + K4, or the
+  depth_pid       (depth.py:213-228) -> K1x fixed-point tcgen05 Gram + K4, or the
                                         exact O(N*M) factorisation K5 + K9
   depth_eid       (depth.py:192-210) -> K6/K7 binary check + pack, K2 exact
                                         integer Gram (tcgen05 kind::i8) + exact
@@ -366,29 +366,115 @@ def _pid_factorized(de: DeviceEnsemble, out: _Out) -> torch.Tensor:
     return buf
 
 
+# Error bound of the fixed-point Gram (gram_fixed.cu header): per cell
+# product, quantisation 2^-32 (a_i + a_j) + 2^-64 and the dropped digit
+# levels 4..6, at most 255^2 (3 * 2^16 + 2 * 2^8 + 1) * 2^-62, wherever both
+# values have non-zero low digits; fp64 folding adds < 1e-13 relative.
+_FX_TAIL = 255.0 ** 2 * (3 * 2 ** 16 + 2 * 2 ** 8 + 1) * 2.0 ** -62
+_FX_REL = 1e-13
+
+# Diagnostics of the last tensor-core PID on this process (read by bench.py):
+# certified bound, members resolved exactly.
+LAST_GRAM_CERT: dict = {}
+
+
+def _gram_depth_bounds(masses, soft, inv, row_plain, col_inv, m, wmax, wmin):
+    """Rigorous per-member bounds on |depth_gram - depth_exact| (in_in and
+    in_out errors propagated from the per-pair Gram bound)."""
+    n = masses.shape[0]
+    A = masses / np.sqrt(wmin * wmax)          # >= sum_x u sqrt(w / wmax)
+    c = soft.astype(np.float64)
+    order = np.argsort(c, kind="stable")
+    cs = c[order]
+    pre = np.concatenate([[0.0], np.cumsum(cs)])
+    pre_inv = np.concatenate([[0.0], np.cumsum(inv[order] * cs)])
+    inv_s = inv[order]
+    suf_inv = np.concatenate([np.cumsum(inv_s[::-1])[::-1], [0.0]])
+    k = np.searchsorted(cs, c, side="right")   # members with c_j <= c_i
+    min_sum = pre[k] + c * (n - k)             # sum_j min(c_i, c_j)
+    min_sum_inv = pre_inv[k] + c * suf_inv[k]  # sum_j inv_j min(c_i, c_j)
+    sinv = float(inv.sum())
+    row_err = wmax * (2.0 ** -32 * (n * A + A.sum()) + n * m * 2.0 ** -64
+                      + _FX_TAIL * min_sum) + _FX_REL * np.abs(row_plain)
+    col_err = wmax * (2.0 ** -32 * (A * sinv + float(inv @ A)) + m * sinv * 2.0 ** -64
+                      + _FX_TAIL * min_sum_inv) + _FX_REL * np.abs(col_inv)
+    return np.maximum(inv * row_err / n, col_err / n)
+
+
+def _clustered(depth, eps):
+    """Members whose interval [d - eps, d + eps] meets another member's:
+    their relative order is not certified."""
+    lo, hi = depth - eps, depth + eps
+    order = np.argsort(lo, kind="stable")
+    flag = np.zeros(depth.shape[0], dtype=bool)
+    start, reach = 0, -np.inf
+    for pos, i in enumerate(order):
+        if lo[i] > reach:
+            if pos - start > 1:
+                flag[order[start:pos]] = True
+            start = pos
+        reach = max(reach, hi[i])
+    if order.shape[0] - start > 1:
+        flag[order[start:]] = True
+    return flag
+
+
 def _pid_gram(de: DeviceEnsemble, out: _Out) -> np.ndarray:
-    """PID from the symmetric N x N Gram on tcgen05 tensor cores (K1 3xTF32),
-    with the row sums and inverse-mass-weighted column sums of G
-    (depth.py:156-160) fused into the Gram epilogue: no N x N matrix in HBM."""
-    if de.dtype_code != N.PIDB_F32:
-        raise ValidationError("the tensor-core Gram takes float32 members")
+    """PID from the symmetric N x N Gram on the tcgen05 int8 tensor cores
+    (K1x: fixed-point digits, exact integer accumulation), with the row sums
+    and inverse-mass-weighted column sums of G (depth.py:156-160) fused into
+    the Gram epilogue: no N x N matrix in HBM.  Then the rank certifier
+    (SURVEY.md §7.3): every member whose depth interval (rigorous Gram error
+    bound) meets another member's is resolved with the exact fp64 path, so
+    the ranks equal the exact ones.  Returns the masses."""
+    from .reduction import pack_fixed
+
     n, dev = de.n, de.device
+    lib = N.load()
     mass = _masses_device(de)
     inv = out.ptrs()[0]
     N.call("pidb_inverse_masses", n, mass.data_ptr(), inv, stream_ptr(dev))
+    soft = torch.zeros(n, dtype=torch.int64, device=dev)
+    q, ldq, wmax = pack_fixed(de, soft)
     rc = _f64(2 * n, dev)
-    ws = de.workspace(N.load().pidb_gram_tf32x3_workspace_bytes(n, de.m))
-    _launch("pidb_gram_tf32x3_sums", de.ptr(), n, de.m, de.ld, de.wptr(), inv, rc.data_ptr(),
+    ws = de.workspace(lib.pidb_gram_fixed_workspace_bytes(n, de.m, 1))
+    _launch("pidb_gram_fixed_sums", q.data_ptr(), n, de.m, ldq, wmax, inv, rc.data_ptr(),
             rc.data_ptr() + 8 * n, ws.data_ptr(), ws.numel(), stream_ptr(dev))
     _allreduce(rc, de)
+    _allreduce(soft, de)
     _, ii, io, d = out.ptrs()
     N.call("pidb_depth_epilogue", N.PIDB_EPI_PID, n, rc.data_ptr(), mass.data_ptr(),
            rc.data_ptr() + 8 * n, inv, ii, io, d, out.rank.data_ptr(), stream_ptr(dev))
-    return mass.cpu().numpy()
+    masses = mass.cpu().numpy()
+    h = out.host()
+    rch = rc.cpu().numpy()
+    wmin = float(de.weights.min()) if de.weights is not None else 1.0
+    if de.process_group is not None:
+        import torch.distributed as dist
 
-
-def _gram_available() -> bool:
-    return N.has_symbol("pidb_gram_tf32x3")
+        t = torch.tensor([wmax, -wmin], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=de.process_group)
+        wmax, wmin = float(t[0]), -float(t[1])
+        mt = torch.tensor([float(de.m)], dtype=torch.float64, device=dev)
+        dist.all_reduce(mt, group=de.process_group)
+        m_cells = float(mt)
+    else:
+        m_cells = float(de.m)
+    eps = _gram_depth_bounds(masses, soft.cpu().numpy(), h[:n], rch[:n], rch[n:], m_cells,
+                             wmax, wmin)
+    flag = _clustered(h[3 * n:4 * n], eps)
+    LAST_GRAM_CERT.clear()
+    LAST_GRAM_CERT.update(max_bound=float(eps.max()), resolved_exactly=int(flag.sum()))
+    if flag.any():
+        exact = _Out(n, dev, extra=2 * n + 1)
+        _pid_factorized(de, exact)
+        e = exact.host()
+        blk = h.copy()
+        for k in (1, 2, 3):
+            blk[k * n:(k + 1) * n][flag] = e[k * n:(k + 1) * n][flag]
+        blk[4 * n:5 * n] = ranks_from_depths(blk[3 * n:4 * n]).view(np.float64)
+        out._host = blk
+    return masses
 
 
 def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") -> DepthResult:
@@ -397,10 +483,11 @@ def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") 
     algorithm="factorized" (default via "auto"): exact fp64 O(N*M) two-pass
     identity (row sums of G against S = sum_j u_j, column sums against
     T = sum_i u_i / m_i); agrees with the reference to ~1e-15.
-    algorithm="gram": the symmetric N x N Gram on tcgen05 tensor cores
-    (3xTF32, fp32 TMEM blocks folded into an fp64 shadow) followed by the
-    row/column-sum epilogue — the reference's own formulation, within the
-    3xTF32 bound (1e-5 relative; K1).
+    algorithm="gram": the symmetric N x N Gram on the tcgen05 int8 tensor
+    cores (fixed-point digits, exact integer accumulation; depth error
+    ~1e-9) followed by the row/column-sum epilogue -- the reference's own
+    formulation -- and a rank certifier that resolves every member whose
+    error interval meets another's with the exact path (K1).
     """
     t0 = time.perf_counter()
     resolve_workers(workers)

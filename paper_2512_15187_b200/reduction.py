@@ -5,7 +5,8 @@ the chunked ``rows . diag(w) . cols^T`` (or ``. (1 - cols)^T``) that
 _pairwise_sums tiles over member blocks (depth.py:122-161).  Here one kernel
 launch computes the whole symmetric N x N Gram of a resident ensemble:
 
-* K1 ``pidb_gram_tf32x3``: fuzzy members, 3xTF32 tcgen05 MMAs, fp64 result;
+* K1x ``pidb_gram_fixed``: fuzzy members as fixed-point base-256 digits,
+  tcgen05 ``kind::i8`` MMAs with exact integer accumulation, fp64 result;
 * K2 ``pidb_gram_i8``: 0/1 members packed to uint8 (K7), exact int64 result;
 * ``pidb_gram_f64``: the array-level ``gram_block`` seam itself, fp64 on the
   CUDA cores (the reference's rtol 1e-12 contract).
@@ -33,18 +34,38 @@ def _allreduce(t: torch.Tensor, de: DeviceEnsemble) -> None:
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=de.process_group)
 
 
-def gram_device(de: DeviceEnsemble) -> torch.Tensor:
-    """G[i, j] = sum_x w(x) u_i(x) u_j(x) as an (n, n) fp64 device tensor."""
-    if de.dtype_code != N.PIDB_F32:
-        raise ValidationError("the tensor-core Gram takes float32 members")
-    lib = N.load()
-    g = torch.empty((de.n, de.n), dtype=torch.float64, device=de.device)
-    wsb = lib.pidb_gram_tf32x3_workspace_bytes(de.n, de.m)
-    ws = de.workspace(wsb)
+def pack_fixed(de: DeviceEnsemble, soft: torch.Tensor | None = None):
+    """K1x pack: members -> fixed-point digit lines for the int8 Gram
+    (pidb_fixed_pack).  Returns (q, ldq, wmax); `soft` (uint64-as-int64 (n,),
+    zero-filled by the caller) receives the per-member soft-cell counts of
+    the certifier's error bound.  The digit buffer is kept on the ensemble
+    (re-packed on every call: the members may change in place)."""
+    ldq = int(N.load().pidb_fixed_ld(de.m))
+    q = de._cache.get("fixed_q")
+    if q is None or q.shape != (de.n, ldq) or torch.cuda.is_current_stream_capturing():
+        q = torch.empty((de.n, ldq), dtype=torch.uint8, device=de.device)
+        if not torch.cuda.is_current_stream_capturing():
+            de._cache["fixed_q"] = q
+    wmax = float(np.max(de.weights.cpu().numpy())) if de.weights is not None else 1.0
     from .depth import _launch
 
-    _launch("pidb_gram_tf32x3", de.ptr(), de.n, de.m, de.ld, de.wptr(), g.data_ptr(),
-           ws.data_ptr(), ws.numel(), stream_ptr(de.device))
+    _launch("pidb_fixed_pack", de.ptr(), de.dtype_code, de.n, de.m, de.ld, de.wptr(), wmax,
+            q.data_ptr(), ldq, None if soft is None else soft.data_ptr(), stream_ptr(de.device))
+    return q, ldq, wmax
+
+
+def gram_device(de: DeviceEnsemble) -> torch.Tensor:
+    """G[i, j] = sum_x w(x) u_i(x) u_j(x) as an (n, n) fp64 device tensor, from
+    the fixed-point int8 tensor-core Gram (exact integer accumulation; error
+    bound in include/pidb.h)."""
+    lib = N.load()
+    q, ldq, wmax = pack_fixed(de)
+    g = torch.empty((de.n, de.n), dtype=torch.float64, device=de.device)
+    ws = de.workspace(lib.pidb_gram_fixed_workspace_bytes(de.n, de.m, 0))
+    from .depth import _launch
+
+    _launch("pidb_gram_fixed", q.data_ptr(), de.n, de.m, ldq, wmax, g.data_ptr(),
+            ws.data_ptr(), ws.numel(), stream_ptr(de.device))
     _allreduce(g, de)
     return g
 

@@ -19,7 +19,7 @@ def header_functions() -> list[str]:
 def test_header_declares_the_hot_path():
     names = header_functions()
     for must in ("pidb_pid_mean_partials", "pidb_pid_colsums", "pidb_member_masses",
-                 "pidb_gram_i8", "pidb_gram_tf32x3", "pidb_depth_epilogue",
+                 "pidb_gram_i8", "pidb_gram_fixed_sums", "pidb_gram_f64", "pidb_depth_epilogue",
                  "pidb_eid_exact_epilogue", "pidb_pair_sums", "pidb_last_error"):
         assert must in names
 

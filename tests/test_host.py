@@ -142,3 +142,23 @@ def test_gen_fuzzy_disk_matches_reference_members():
         assert np.array_equal(pb.gen_fuzzy_disk(g, (cy, cx), r, sigma2).values, z["U"][i])
     with pytest.raises(pb.ValidationError):
         pb.gen_fuzzy_disk(pb.GridSpec((4,)), (0, 0), 1.0, 1.0)
+
+
+def test_gram_certifier_host_logic():
+    """Rank certifier of the tensor-core PID (depth._clustered /
+    _gram_depth_bounds): overlapping error intervals are flagged as whole
+    clusters, separated members are not; the bound grows with the soft-cell
+    counts and vanishes for exact (digit-free) members."""
+    from paper_2512_15187_b200.depth import _clustered, _gram_depth_bounds
+
+    d = np.array([0.5, 0.1, 0.30, 0.3000001, 0.9, 0.2999999])
+    eps = np.full(6, 1e-6)
+    np.testing.assert_array_equal(_clustered(d, eps), [False, False, True, True, False, True])
+    assert not _clustered(d, np.full(6, 1e-8)).any()
+    assert _clustered(np.array([0.2, 0.2]), np.zeros(2)).all()  # exact tie
+    m = np.array([10.0, 20.0, 30.0])
+    inv = 1.0 / m
+    rp, ci = np.array([30.0, 60.0, 90.0]), np.array([3.0, 3.0, 3.0])
+    e0 = _gram_depth_bounds(m, np.zeros(3, dtype=np.int64), inv, rp, ci, 100.0, 1.0, 1.0)
+    e1 = _gram_depth_bounds(m, np.array([50, 60, 70]), inv, rp, ci, 100.0, 1.0, 1.0)
+    assert (e0 < 1e-9).all() and (e1 > e0).all() and (e1 < 1e-6).all()
