@@ -129,16 +129,22 @@ int pidb_gram_i8(const uint8_t* b, int64_t n, int64_t m, int64_t ldb,
  * depth.py:122-161 / reduction.py:75-97; DESIGN.md §3 K1).
  *
  * pidb_fixed_pack: a = u * sqrt(w / wmax) (w nullable: a = u), values in
- * [0, 1]; q = rint(a 2^31) as four base-256 digits, stored per 32-cell block
- * as one 128-byte line [d0 x32 | d1 x32 | d2 x32 | d3 x32]; ldq >=
- * pidb_fixed_ld(m) bytes, a multiple of 128, q 128-byte aligned.
+ * [0, 1]; q = rint(a 2^31) as four base-256 digits.  Layout of q
+ * (pidb_fixed_bytes(n, m) bytes, 1 KB aligned; rows past n must be zero, so
+ * zero-fill it once): 16 KB tiles [ceil(n/128) row blocks][ceil(m/32) cell
+ * blocks], each 128 member lines of 128 bytes [d0 x32 | d1 x32 | d2 x32 |
+ * d3 x32] in the 128-byte-swizzled K-major order of tcgen05 (16-byte chunk c
+ * of line r at chunk c ^ (r % 8)).  ld % 4 == 0, u 16-byte aligned.
  * soft_count[i] (nullable, zero-filled by the caller) += cells of member i
  * whose q has non-zero low 24 bits (the only cells with a truncation tail;
- * used by the rank certifier's error bound). */
-int64_t pidb_fixed_ld(int64_t m);
+ * used by the rank certifier's error bound).  mass (nullable) receives the
+ * member masses sum_x w u_i (depth.py:88-102) from the same pass, fp64 in a
+ * fixed order; it needs a workspace of pidb_fixed_pack_workspace_bytes. */
+size_t pidb_fixed_bytes(int64_t n, int64_t m);
+size_t pidb_fixed_pack_workspace_bytes(int64_t n, int64_t m);
 int pidb_fixed_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
-                    const double* w, double wmax, uint8_t* q, int64_t ldq,
-                    uint64_t* soft_count, void* stream);
+                    const double* w, double wmax, uint8_t* q, uint64_t* soft_count,
+                    double* mass, void* ws, size_t ws_bytes, void* stream);
 /* G[i*n+j] = wmax * 2^-62 * sum_x (digit-pair levels 0..3 of q_i q_j): every
  * product accumulates exactly (int32 TMEM, folded into fp64 every 8192
  * cells); |G - G_exact| <= wmax (2^-32 (A_i + A_j) + m 2^-64 +
@@ -146,12 +152,12 @@ int pidb_fixed_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
  * `sums` selects the workspace of pidb_gram_fixed_sums (1) or of the full
  * Gram (0). */
 size_t pidb_gram_fixed_workspace_bytes(int64_t n, int64_t m, int sums);
-int pidb_gram_fixed(const uint8_t* q, int64_t n, int64_t m, int64_t ldq, double wmax,
-                    double* gram, void* ws, size_t ws_bytes, void* stream);
+int pidb_gram_fixed(const uint8_t* q, int64_t n, int64_t m, double wmax, double* gram,
+                    void* ws, size_t ws_bytes, void* stream);
 /* The PID sums of the same Gram fused into the tile epilogue (no n x n
  * matrix in HBM): row_plain[i] = sum_j G[i,j], col_inv[i] = sum_j inv_j
  * G[i,j] (depth.py:155-160, G symmetric); additive over cell shards. */
-int pidb_gram_fixed_sums(const uint8_t* q, int64_t n, int64_t m, int64_t ldq, double wmax,
+int pidb_gram_fixed_sums(const uint8_t* q, int64_t n, int64_t m, double wmax,
                          const double* inv, double* row_plain, double* col_inv, void* ws,
                          size_t ws_bytes, void* stream);
 

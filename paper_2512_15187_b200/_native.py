@@ -55,11 +55,12 @@ SIGNATURES: dict[str, tuple] = {
     "pidb_gram_i8_workspace_bytes": (_sz, [_i64, _i64]),
     "pidb_gram_i8": (_int, [_p, _i64, _i64, _i64, _p, _p, _sz, _p]),
     "pidb_gram_reduce": (_int, [_p, _i64, _p, _p, _p, _p]),
-    "pidb_fixed_ld": (_i64, [_i64]),
-    "pidb_fixed_pack": (_int, [_p, _int, _i64, _i64, _i64, _p, _dbl, _p, _i64, _p, _p]),
+    "pidb_fixed_bytes": (_sz, [_i64, _i64]),
+    "pidb_fixed_pack_workspace_bytes": (_sz, [_i64, _i64]),
+    "pidb_fixed_pack": (_int, [_p, _int, _i64, _i64, _i64, _p, _dbl, _p, _p, _p, _p, _sz, _p]),
     "pidb_gram_fixed_workspace_bytes": (_sz, [_i64, _i64, _int]),
-    "pidb_gram_fixed": (_int, [_p, _i64, _i64, _i64, _dbl, _p, _p, _sz, _p]),
-    "pidb_gram_fixed_sums": (_int, [_p, _i64, _i64, _i64, _dbl, _p, _p, _p, _p, _sz, _p]),
+    "pidb_gram_fixed": (_int, [_p, _i64, _i64, _dbl, _p, _p, _sz, _p]),
+    "pidb_gram_fixed_sums": (_int, [_p, _i64, _i64, _dbl, _p, _p, _p, _p, _sz, _p]),
     "pidb_gram_f64_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "pidb_gram_f64": (_int, [_p, _p, _int, _i64, _i64, _i64, _i64, _i64, _p, _int, _p, _p, _sz,
                              _p]),

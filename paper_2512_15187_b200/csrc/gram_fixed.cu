@@ -12,11 +12,15 @@
 // Representation (pidb_fixed_pack, one HBM pass): every member value u in
 // [0, 1] (times sqrt(w / w_max) on weighted grids, so that G = w_max * sum
 // a_i a_j) becomes q = rint(a * 2^31) <= 2^31, split into four base-256
-// digits d0 (0..128), d1, d2, d3.  Per 32-cell block a member row stores the
-// digits plane by plane: [d0 x32 | d1 x32 | d2 x32 | d3 x32] = one 128-byte
-// line, so a TMA box of 128 rows x 128 bytes with SWIZZLE_128B is directly
-// the K-major operand of tcgen05.mma.kind::i8 (K = 32) and digit plane k of
-// it is the same descriptor advanced by 32 bytes.
+// digits d0 (0..128), d1, d2, d3.  Per 32-cell block a member stores its
+// digits plane by plane, [d0 x32 | d1 x32 | d2 x32 | d3 x32] = one 128-byte
+// line, and the lines of 128 members (a row block) for one cell block form
+// one contiguous 16 KB tile already in the 128-byte-swizzled K-major order
+// the tensor core reads (16-byte chunk c of line r at chunk c ^ (r % 8)):
+// a stage is one or two plain 1D bulk copies (full DRAM bursts, unlike a
+// 2D box of 128-byte rows strided by the member pitch), digit plane k is
+// the operand descriptor advanced by 32 bytes.  Tiles are ordered
+// [row block][cell block], so a row block's stream is sequential.
 //
 // Products: q_i q_j = 2^24 * sum_s 2^(8(3-s)) L_s with L_s = sum_{k+l=s}
 // d_k e_l; the levels s = 0..3 (10 digit pairs) are kept, the dropped
@@ -38,6 +42,7 @@
 // the two column counterparts; fixed-order reductions finish both.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "tcgen05.cuh"
 
@@ -58,6 +63,8 @@ constexpr double kTwoPow31 = 2147483648.0;
 
 struct FxParams {
   int n, nib, ntiles, splits, kblocks, kb_per;
+  int flush;          // stages per int32 window (kFlush; A/B hook PIDB_FX_FLUSH)
+  int noload;         // A/B hook PIDB_FX_NOLOAD=1: skip the TMA loads (timing only)
   int sums;           // 1: tile sums (PID), 0: fp64 tiles
   const double* inv;  // sums: inverse masses (n)
   double* part;       // sums: [units][4][kB]; tiles: [units][kB][kB]
@@ -72,48 +79,148 @@ __host__ __device__ __forceinline__ void fx_tile(int t, int& ib, int& jb) {
 }
 
 // ---------------------------------------------------------------- packing
-// One warp per (member row, segment of 64 blocks of 32 cells); lane = cell.
+// One CTA (8 warps) per (group of 8 members = one 1 KB swizzle atom of every
+// tile, segment of 128 cell blocks); warp w owns member 8g + w.  Per
+// iteration a warp takes 128 cells (4 blocks): lane L loads cells 4L..4L+3
+// with one 128-bit load, and its four digit-k bytes are exactly word L % 8
+// of plane k of block L / 8 (no shuffles).  The words are staged in shared
+// memory in the swizzled tile order and leave as 16-byte stores: per block
+// the 8 members' lines are one contiguous 1 KB atom.
+__device__ __forceinline__ uint32_t fx_quant(double a) {
+  const uint32_t q = (uint32_t)__double2uint_rn(a * kTwoPow31);
+  return min(q, 0x80000000u);
+}
+
 template <typename T>
-__global__ void __launch_bounds__(256)
+struct Vec4;
+template <>
+struct Vec4<float> {
+  float4 v;
+  __device__ __forceinline__ double operator[](int e) const {
+    return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+  }
+};
+template <>
+struct Vec4<double> {
+  double2 a, b;
+  __device__ __forceinline__ double operator[](int e) const {
+    return e == 0 ? a.x : e == 1 ? a.y : e == 2 ? b.x : b.y;
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ Vec4<T> fx_load4(const T* __restrict__ src, int64_t x, int64_t m) {
+  Vec4<T> r;
+  if (x + 3 < m) {
+    if constexpr (sizeof(T) == 4) {
+      r.v = __ldcs(reinterpret_cast<const float4*>(src + x));
+    } else {
+      r.a = __ldcs(reinterpret_cast<const double2*>(src + x));
+      r.b = __ldcs(reinterpret_cast<const double2*>(src + x + 2));
+    }
+  } else {
+    T t[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) t[e] = x + e < m ? src[x + e] : T(0);
+    if constexpr (sizeof(T) == 4) {
+      r.v = make_float4(t[0], t[1], t[2], t[3]);
+    } else {
+      r.a = make_double2(t[0], t[1]);
+      r.b = make_double2(t[2], t[3]);
+    }
+  }
+  return r;
+}
+
+constexpr int kPackSeg = 128;   // cell blocks per CTA unit
+constexpr int kPackIter = 16;   // cell blocks per CTA iteration (4 loads in flight per lane)
+
+template <typename T>
+__global__ void __launch_bounds__(256, 3)
     fx_pack_kernel(const T* __restrict__ u, int64_t ld, int n, int64_t m,
                    const double* __restrict__ w, double inv_wmax, uint8_t* __restrict__ q,
-                   int64_t ldq, int64_t nblk, int64_t nseg, unsigned long long* __restrict__ soft) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int k = lane >> 3, wi = lane & 7;
-  for (int64_t unit = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       unit < (int64_t)n * nseg; unit += warps) {
-    const int64_t row = unit / nseg, seg = unit - row * nseg;
-    const int64_t b0 = seg * 64, b1 = min(nblk, b0 + 64);
-    const T* src = u + row * ld;
-    uint32_t* dst = reinterpret_cast<uint32_t*>(q + row * ldq);
+                   int64_t nblk, int64_t nseg, unsigned long long* __restrict__ soft,
+                   double* __restrict__ mpart) {
+  __shared__ __align__(16) uint32_t stage[kPackIter][8][32];  // [block][member line][word]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane >> 3, wi = lane & 7;
+  const int64_t ngrp = (n + 7) / 8;
+  for (int64_t unit = blockIdx.x; unit < ngrp * nseg; unit += gridDim.x) {
+    const int64_t grp = unit / nseg, seg = unit - grp * nseg;
+    const int64_t row = grp * 8 + warp;
+    const bool live = row < n;
+    const int64_t b0 = seg * kPackSeg, b1 = min(nblk, b0 + kPackSeg);
+    const T* src = u + (live ? row : 0) * ld;
+    const int r8 = (int)(grp & 15) * 8;  // first line of the group inside its tile
+    // atom of this group in tile (row block, block): lines r8 .. r8 + 7
+    uint8_t* atom0 = q + ((grp / 16) * nblk) * (int64_t)kTileBytes + r8 * kLine;
     unsigned int cnt = 0;
-#pragma unroll 4
-    for (int64_t b = b0; b < b1; ++b) {
-      const int64_t x = b * kCellsPerStage + lane;
-      double a = 0.0;
-      if (x < m) {
-        a = (double)src[x];
-        if (w) a *= sqrt(w[x] * inv_wmax);
-      }
-      uint32_t qq = (uint32_t)__double2uint_rn(a * kTwoPow31);
-      qq = min(qq, 0x80000000u);
-      // byte k of `packed` = digit k (most significant first)
-      const uint32_t packed = (qq >> 24) | (((qq >> 16) & 255u) << 8) | (((qq >> 8) & 255u) << 16) |
-                              ((qq & 255u) << 24);
-      cnt += __popc(__ballot_sync(0xffffffffu, (qq & 0xFFFFFFu) != 0u));
-      // lane L writes word L of the 128-byte line: plane k = L / 8, cells
-      // 4 (L % 8) .. +3 -> digit k of lanes 4 wi .. 4 wi + 3
-      uint32_t word = 0;
+    double mass = 0.0;  // sum w u of this lane's cells (fp64, fixed order)
+    for (int64_t b = b0; b < b1; b += kPackIter) {
+      Vec4<T> v[kPackIter / 4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const uint32_t s = __shfl_sync(0xffffffffu, packed, 4 * wi + t);
-        word |= ((s >> (8 * k)) & 255u) << (8 * t);
+      for (int j = 0; j < kPackIter / 4; ++j) {
+        const int64_t x = (b + 4 * j + sub) * kCellsPerStage + 4 * wi;
+        if (live) v[j] = fx_load4(src, x, m);
+        else v[j] = fx_load4(src, x, 0);
       }
-      dst[b * (kLine / 4) + lane] = word;
+#pragma unroll
+      for (int j = 0; j < kPackIter / 4; ++j) {
+        const int64_t x = (b + 4 * j + sub) * kCellsPerStage + 4 * wi;
+        uint32_t d[4] = {0u, 0u, 0u, 0u};  // plane words: byte e = digit of cell x + e
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          double a = v[j][e];
+          if (w && x + e < m) {
+            const double wx = __ldcs(w + x + e);
+            mass = fma(wx, a, mass);
+            a *= sqrt(wx * inv_wmax);
+          } else {
+            mass += a;
+          }
+          const uint32_t qq = fx_quant(a);
+          cnt += (qq & 0xFFFFFFu) != 0u;
+          d[0] |= (qq >> 24) << (8 * e);
+          d[1] |= ((qq >> 16) & 255u) << (8 * e);
+          d[2] |= ((qq >> 8) & 255u) << (8 * e);
+          d[3] |= (qq & 255u) << (8 * e);
+        }
+        // line r = r8 + warp: byte 32k + 4wi -> chunk (2k + wi/4) ^ (r % 8) = ^ warp
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          stage[4 * j + sub][warp][((((2 * k + (wi >> 2)) ^ warp) & 7) << 2) + (wi & 3)] = d[k];
+      }
+      __syncthreads();
+      // kPackIter blocks x 1 KB atoms, 16 bytes per thread and store
+#pragma unroll
+      for (int t = threadIdx.x; t < kPackIter * 64; t += 256) {
+        const int blk_t = t >> 6, off = (t & 63) * 16;
+        if (b + blk_t < b1)
+          *reinterpret_cast<uint4*>(atom0 + (b + blk_t) * (int64_t)kTileBytes + off) =
+              reinterpret_cast<const uint4*>(&stage[blk_t][0][0])[t & 63];
+      }
+      __syncthreads();
     }
-    if (soft && lane == 0 && cnt) atomicAdd(soft + row, (unsigned long long)cnt);
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (soft && live && lane == 0 && cnt) atomicAdd(soft + row, (unsigned long long)cnt);
+    if (mpart) {
+      mass = warp_sum(mass);
+      if (live && lane == 0) mpart[row * nseg + seg] = mass;
+    }
   }
+}
+
+// masses[i] = sum over segments of the pack's per-(member, segment) partials,
+// in segment order (deterministic).
+__global__ void fx_mass_reduce_kernel(const double* __restrict__ mpart, int n, int64_t nseg,
+                                      double* __restrict__ mass) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int64_t k = lane; k < nseg; k += 32) s += mpart[(int64_t)row * nseg + k];
+  s = warp_sum(s);
+  if (lane == 0) mass[row] = s;
 }
 
 // ------------------------------------------------------------------- Gram
@@ -122,7 +229,7 @@ __device__ __forceinline__ void epi_sync() {  // the 16 epilogue warps only
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    gram_fx_kernel(const __grid_constant__ CUtensorMap tmap, const FxParams p) {
+    gram_fx_kernel(const uint8_t* __restrict__ qd, const FxParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   unsigned char* ring = smem_raw + pad;
@@ -140,10 +247,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool diag = ib == jb;
   const int kb0 = split * p.kb_per;
   const int nk = max(0, min(p.kblocks, kb0 + p.kb_per) - kb0);
-  const int nflush = (nk + kFlush - 1) / kFlush;
+  const int fl = p.flush;
+  const int nflush = (nk + fl - 1) / fl;
 
   if (threadIdx.x == 0) {
-    prefetch_tma_desc(&tmap);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -167,10 +274,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int k = 0; k < nk; ++k) {
         mbar_wait(&empty[s], ph ^ 1u);
         unsigned char* a = ring + s * kStageBytes;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        const int x = (kb0 + k) * kLine;
-        tma_load_2d(a, &tmap, x, ib * kB, &full[s], pol);
-        if (!diag) tma_load_2d(a + kTileBytes, &tmap, x, jb * kB, &full[s], pol);
+        if (p.noload) {
+          mbar_arrive(&full[s]);
+        } else {
+          mbar_arrive_expect_tx(&full[s], bytes);
+          const int64_t kb = kb0 + k;
+          bulk_load(a, qd + ((int64_t)ib * p.kblocks + kb) * kTileBytes, kTileBytes, &full[s], pol);
+          if (!diag)
+            bulk_load(a + kTileBytes, qd + ((int64_t)jb * p.kblocks + kb) * kTileBytes, kTileBytes,
+                      &full[s], pol);
+        }
         if (++s == kStages) { s = 0; ph ^= 1u; }
       }
     }
@@ -179,9 +292,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int k = 0; k < nk; ++k) {
-        const int kw = k % kFlush;
+        const int kw = k % fl;
         if (kw == 0 && k > 0) {
-          mbar_wait(tempty, (uint32_t)((k / kFlush - 1) & 1));  // epilogue drained TMEM
+          mbar_wait(tempty, (uint32_t)((k / fl - 1) & 1));  // epilogue drained TMEM
           tc::fence_after();
         }
         mbar_wait(&full[s], ph);
@@ -199,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mma_i8(tmem + 128u * lv, da + 2 * dk, db + 2 * (lv - dk), kIdesc,
                        dk != 0 ? 1u : acc);
         tc::commit(&empty[s]);
-        if (kw == kFlush - 1 || k == nk - 1) tc::commit(tfull);
+        if (kw == fl - 1 || k == nk - 1) tc::commit(tfull);
         if (++s == kStages) { s = 0; ph ^= 1u; }
       }
     }
@@ -345,17 +458,16 @@ FxPlan plan_fx(int64_t n, int64_t m) {
   return g;
 }
 
-int launch_gram_fx(const uint8_t* qd, int64_t n, int64_t m, int64_t ldq, const FxPlan& g,
-                   FxParams prm, cudaStream_t st) {
-  CUtensorMap tm;
-  int rc = encode_tma_2d(&tm, qd, CU_TENSOR_MAP_DATA_TYPE_UINT8, (uint64_t)ldq, (uint64_t)n,
-                         (uint64_t)ldq, kLine, kB, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (rc != PIDB_OK) return rc;
+int launch_gram_fx(const uint8_t* qd, int64_t n, const FxPlan& g, FxParams prm,
+                   cudaStream_t st) {
   prm.n = (int)n; prm.nib = g.nib; prm.ntiles = g.ntiles; prm.splits = g.splits;
   prm.kblocks = g.kblocks; prm.kb_per = g.kb_per;
+  prm.flush = kFlush;
+  if (const char* e = getenv("PIDB_FX_FLUSH")) prm.flush = std::max(1, atoi(e));
+  prm.noload = getenv("PIDB_FX_NOLOAD") != nullptr && atoi(getenv("PIDB_FX_NOLOAD")) != 0;
   PIDB_CUDA(cudaFuncSetAttribute(gram_fx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)g.smem));
-  gram_fx_kernel<<<g.units, kThreads, g.smem, st>>>(tm, prm);
+  gram_fx_kernel<<<g.units, kThreads, g.smem, st>>>(qd, prm);
   PIDB_LAUNCH_CHECK("gram_fx_kernel");
   return PIDB_OK;
 }
@@ -365,34 +477,51 @@ int launch_gram_fx(const uint8_t* qd, int64_t n, int64_t m, int64_t ldq, const F
 
 using namespace pidb;
 
-extern "C" int64_t pidb_fixed_ld(int64_t m) {
-  return m < 1 ? 0 : (m + kCellsPerStage - 1) / kCellsPerStage * kLine;
+extern "C" size_t pidb_fixed_bytes(int64_t n, int64_t m) {
+  if (n < 1 || m < 1) return 0;
+  return (size_t)((n + kB - 1) / kB) * (size_t)((m + kCellsPerStage - 1) / kCellsPerStage) *
+         kTileBytes;
+}
+
+extern "C" size_t pidb_fixed_pack_workspace_bytes(int64_t n, int64_t m) {
+  if (n < 1 || m < 1) return 0;
+  const int64_t nblk = (m + kCellsPerStage - 1) / kCellsPerStage;
+  return 256 + (size_t)n * ((nblk + kPackSeg - 1) / kPackSeg) * sizeof(double);
 }
 
 extern "C" int pidb_fixed_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
-                               const double* w, double wmax, uint8_t* q, int64_t ldq,
-                               uint64_t* soft_count, void* stream) {
+                               const double* w, double wmax, uint8_t* q, uint64_t* soft_count,
+                               double* mass, void* ws, size_t ws_bytes, void* stream) {
   PIDB_REQUIRE(u && q && n >= 1 && m >= 1 && ld >= m, "bad arguments to pidb_fixed_pack");
   PIDB_REQUIRE(dtype == PIDB_F32 || dtype == PIDB_F64, "unknown dtype %d", dtype);
-  PIDB_REQUIRE(ldq >= pidb_fixed_ld(m) && ldq % kLine == 0 &&
-                   (reinterpret_cast<uintptr_t>(q) & 127) == 0,
-               "digit rows need ldq >= pidb_fixed_ld(m), a multiple of 128, 128-byte aligned");
+  PIDB_REQUIRE(ld % 4 == 0 && (reinterpret_cast<uintptr_t>(u) & 15) == 0,
+               "member rows must be 16-byte aligned with ld a multiple of 4");
+  PIDB_REQUIRE((reinterpret_cast<uintptr_t>(q) & 1023) == 0, "digit tiles must be 1 KB aligned");
   PIDB_REQUIRE(!w || wmax > 0.0, "weighted packing needs wmax > 0");
+  PIDB_REQUIRE(!mass || (ws && ws_bytes >= pidb_fixed_pack_workspace_bytes(n, m)),
+               "workspace too small: need %zu bytes", pidb_fixed_pack_workspace_bytes(n, m));
+  double* mpart = mass ? reinterpret_cast<double*>(static_cast<char*>(ws) + 256) : nullptr;
   const int64_t nblk = (m + kCellsPerStage - 1) / kCellsPerStage;
-  const int64_t nseg = (nblk + 63) / 64;
-  const int64_t warps = n * nseg;
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 16));
+  const int64_t nseg = (nblk + kPackSeg - 1) / kPackSeg;
+  const int64_t units = (n + 7) / 8 * nseg;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(units, 148 * 3));
   cudaStream_t st = (cudaStream_t)stream;
   const double iw = w ? 1.0 / wmax : 1.0;
   if (dtype == PIDB_F32)
     fx_pack_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(u), ld, (int)n, m, w,
-                                                  iw, q, ldq, nblk, nseg,
-                                                  reinterpret_cast<unsigned long long*>(soft_count));
+                                                  iw, q, nblk, nseg,
+                                                  reinterpret_cast<unsigned long long*>(soft_count),
+                                                  mpart);
   else
     fx_pack_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(u), ld, (int)n, m, w,
-                                                   iw, q, ldq, nblk, nseg,
-                                                   reinterpret_cast<unsigned long long*>(soft_count));
+                                                   iw, q, nblk, nseg,
+                                                   reinterpret_cast<unsigned long long*>(soft_count),
+                                                   mpart);
   PIDB_LAUNCH_CHECK("fx_pack_kernel");
+  if (mass) {
+    fx_mass_reduce_kernel<<<(int)((n + 7) / 8), 256, 0, st>>>(mpart, (int)n, nseg, mass);
+    PIDB_LAUNCH_CHECK("fx_mass_reduce_kernel");
+  }
   return PIDB_OK;
 }
 
@@ -402,19 +531,17 @@ extern "C" size_t pidb_gram_fixed_workspace_bytes(int64_t n, int64_t m, int sums
   return sums ? g.ws_sums : g.ws_tiles;
 }
 
-static int fx_check(const uint8_t* q, int64_t n, int64_t m, int64_t ldq) {
+static int fx_check(const uint8_t* q, int64_t n, int64_t m) {
   PIDB_REQUIRE(q && n >= 1 && m >= 1, "bad arguments to the fixed-point Gram");
-  PIDB_REQUIRE(ldq >= pidb_fixed_ld(m) && ldq % kLine == 0 &&
-                   (reinterpret_cast<uintptr_t>(q) & 127) == 0,
-               "digit rows need ldq >= pidb_fixed_ld(m), a multiple of 128, 128-byte aligned");
+  PIDB_REQUIRE((reinterpret_cast<uintptr_t>(q) & 1023) == 0, "digit tiles must be 1 KB aligned");
   PIDB_REQUIRE(n <= (1 << 20), "too many members for the Gram");
   PIDB_REQUIRE(m < ((int64_t)1 << 40), "too many cells");
   return PIDB_OK;
 }
 
-extern "C" int pidb_gram_fixed(const uint8_t* q, int64_t n, int64_t m, int64_t ldq, double wmax,
-                               double* gram, void* ws, size_t ws_bytes, void* stream) {
-  int rc = fx_check(q, n, m, ldq);
+extern "C" int pidb_gram_fixed(const uint8_t* q, int64_t n, int64_t m, double wmax, double* gram,
+                               void* ws, size_t ws_bytes, void* stream) {
+  int rc = fx_check(q, n, m);
   if (rc != PIDB_OK) return rc;
   PIDB_REQUIRE(gram, "null output");
   const FxPlan g = plan_fx(n, m);
@@ -423,7 +550,7 @@ extern "C" int pidb_gram_fixed(const uint8_t* q, int64_t n, int64_t m, int64_t l
   prm.sums = 0;
   prm.part = reinterpret_cast<double*>(static_cast<char*>(ws) + 256);
   cudaStream_t st = (cudaStream_t)stream;
-  rc = launch_gram_fx(q, n, m, ldq, g, prm, st);
+  rc = launch_gram_fx(q, n, g, prm, st);
   if (rc != PIDB_OK) return rc;
   const double scale = wmax * std::ldexp(1.0, -38);
   const int64_t total = n * n;
@@ -433,10 +560,10 @@ extern "C" int pidb_gram_fixed(const uint8_t* q, int64_t n, int64_t m, int64_t l
   return PIDB_OK;
 }
 
-extern "C" int pidb_gram_fixed_sums(const uint8_t* q, int64_t n, int64_t m, int64_t ldq,
-                                    double wmax, const double* inv, double* row_plain,
-                                    double* col_inv, void* ws, size_t ws_bytes, void* stream) {
-  int rc = fx_check(q, n, m, ldq);
+extern "C" int pidb_gram_fixed_sums(const uint8_t* q, int64_t n, int64_t m, double wmax,
+                                    const double* inv, double* row_plain, double* col_inv,
+                                    void* ws, size_t ws_bytes, void* stream) {
+  int rc = fx_check(q, n, m);
   if (rc != PIDB_OK) return rc;
   PIDB_REQUIRE(inv && row_plain && col_inv, "null inverse masses or outputs");
   const FxPlan g = plan_fx(n, m);
@@ -446,7 +573,7 @@ extern "C" int pidb_gram_fixed_sums(const uint8_t* q, int64_t n, int64_t m, int6
   prm.inv = inv;
   prm.part = reinterpret_cast<double*>(static_cast<char*>(ws) + 256);
   cudaStream_t st = (cudaStream_t)stream;
-  rc = launch_gram_fx(q, n, m, ldq, g, prm, st);
+  rc = launch_gram_fx(q, n, g, prm, st);
   if (rc != PIDB_OK) return rc;
   const double scale = wmax * std::ldexp(1.0, -38);
   fx_sums_reduce_kernel<<<(int)((n + 127) / 128), 128, 0, st>>>(prm.part, (int)n, g.nib, g.ntiles,

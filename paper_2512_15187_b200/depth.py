@@ -431,14 +431,16 @@ def _pid_gram(de: DeviceEnsemble, out: _Out) -> np.ndarray:
 
     n, dev = de.n, de.device
     lib = N.load()
-    mass = _masses_device(de)
+    # one pass: digit tiles, soft-cell counts and the member masses
+    soft = torch.zeros(n, dtype=torch.int64, device=dev)
+    mass = _f64(n, dev)
+    q, wmax = pack_fixed(de, soft, mass)
+    _allreduce(mass, de)
     inv = out.ptrs()[0]
     N.call("pidb_inverse_masses", n, mass.data_ptr(), inv, stream_ptr(dev))
-    soft = torch.zeros(n, dtype=torch.int64, device=dev)
-    q, ldq, wmax = pack_fixed(de, soft)
     rc = _f64(2 * n, dev)
     ws = de.workspace(lib.pidb_gram_fixed_workspace_bytes(n, de.m, 1))
-    _launch("pidb_gram_fixed_sums", q.data_ptr(), n, de.m, ldq, wmax, inv, rc.data_ptr(),
+    _launch("pidb_gram_fixed_sums", q.data_ptr(), n, de.m, wmax, inv, rc.data_ptr(),
             rc.data_ptr() + 8 * n, ws.data_ptr(), ws.numel(), stream_ptr(dev))
     _allreduce(rc, de)
     _allreduce(soft, de)

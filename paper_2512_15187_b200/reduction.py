@@ -34,24 +34,37 @@ def _allreduce(t: torch.Tensor, de: DeviceEnsemble) -> None:
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=de.process_group)
 
 
-def pack_fixed(de: DeviceEnsemble, soft: torch.Tensor | None = None):
-    """K1x pack: members -> fixed-point digit lines for the int8 Gram
-    (pidb_fixed_pack).  Returns (q, ldq, wmax); `soft` (uint64-as-int64 (n,),
+def pack_fixed(de: DeviceEnsemble, soft: torch.Tensor | None = None,
+               mass: torch.Tensor | None = None):
+    """K1x pack: members -> fixed-point digit tiles for the int8 Gram
+    (pidb_fixed_pack).  Returns (q, wmax); `soft` (uint64-as-int64 (n,),
     zero-filled by the caller) receives the per-member soft-cell counts of
-    the certifier's error bound.  The digit buffer is kept on the ensemble
-    (re-packed on every call: the members may change in place)."""
-    ldq = int(N.load().pidb_fixed_ld(de.m))
+    the certifier's error bound, `mass` (fp64 (n,)) the member masses from
+    the same pass.  The digit buffer (zero-filled once: rows
+    past n stay zero) is kept on the ensemble and re-packed on every call
+    (the members may change in place)."""
+    nbytes = int(N.load().pidb_fixed_bytes(de.n, de.m))
     q = de._cache.get("fixed_q")
-    if q is None or q.shape != (de.n, ldq) or torch.cuda.is_current_stream_capturing():
-        q = torch.empty((de.n, ldq), dtype=torch.uint8, device=de.device)
-        if not torch.cuda.is_current_stream_capturing():
-            de._cache["fixed_q"] = q
-    wmax = float(np.max(de.weights.cpu().numpy())) if de.weights is not None else 1.0
+    if q is None or q.numel() != nbytes:
+        buf = torch.zeros(nbytes + 1024, dtype=torch.uint8, device=de.device)
+        off = (-buf.data_ptr()) % 1024  # 1 KB aligned tiles (swizzle atoms)
+        q = buf[off:off + nbytes]
+        de._cache["fixed_q"] = q
+    wmax = de._cache.get("fixed_wmax")
+    if wmax is None:
+        wmax = float(de.weights.max()) if de.weights is not None else 1.0
+        de._cache["fixed_wmax"] = wmax
     from .depth import _launch
 
+    ws = None
+    if mass is not None:
+        ws = torch.empty(int(N.load().pidb_fixed_pack_workspace_bytes(de.n, de.m)),
+                         dtype=torch.uint8, device=de.device)
     _launch("pidb_fixed_pack", de.ptr(), de.dtype_code, de.n, de.m, de.ld, de.wptr(), wmax,
-            q.data_ptr(), ldq, None if soft is None else soft.data_ptr(), stream_ptr(de.device))
-    return q, ldq, wmax
+            q.data_ptr(), None if soft is None else soft.data_ptr(),
+            None if mass is None else mass.data_ptr(), None if ws is None else ws.data_ptr(),
+            0 if ws is None else ws.numel(), stream_ptr(de.device))
+    return q, wmax
 
 
 def gram_device(de: DeviceEnsemble) -> torch.Tensor:
@@ -59,12 +72,12 @@ def gram_device(de: DeviceEnsemble) -> torch.Tensor:
     the fixed-point int8 tensor-core Gram (exact integer accumulation; error
     bound in include/pidb.h)."""
     lib = N.load()
-    q, ldq, wmax = pack_fixed(de)
+    q, wmax = pack_fixed(de)
     g = torch.empty((de.n, de.n), dtype=torch.float64, device=de.device)
     ws = de.workspace(lib.pidb_gram_fixed_workspace_bytes(de.n, de.m, 0))
     from .depth import _launch
 
-    _launch("pidb_gram_fixed", q.data_ptr(), de.n, de.m, ldq, wmax, g.data_ptr(),
+    _launch("pidb_gram_fixed", q.data_ptr(), de.n, de.m, wmax, g.data_ptr(),
             ws.data_ptr(), ws.numel(), stream_ptr(de.device))
     _allreduce(g, de)
     return g

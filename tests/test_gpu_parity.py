@@ -99,6 +99,40 @@ def test_fixed_gram_within_bound(pb, n, m, weighted):
     assert np.array_equal(gram_device(de).cpu().numpy(), got)
 
 
+@pytest.mark.parametrize("n,m,weighted,f64", [(3, 5, False, False), (130, 4100, True, False),
+                                              (9, 333, False, True), (17, 70001, True, True)])
+def test_fixed_pack_layout_masses_soft(pb, n, m, weighted, f64):
+    """K1x pack: the digit tiles decode (swizzle undone) to q = rint(a 2^31)
+    of every member, padding rows/cells are zero, the fused masses equal the
+    fp64 sums (and K6's within 1e-13 relative), soft counts are exact."""
+    from paper_2512_15187_b200.depth import _masses_device
+    from paper_2512_15187_b200.reduction import pack_fixed
+
+    U, w = make_fuzzy(n * 3 + m, n, (m,), weighted)
+    if f64:
+        U = U.astype(np.float64) ** 1.5
+    de = pb.stage(pb.Ensemble(pb.GridSpec((m,), w), [pb.ProbMask(pb.GridSpec((m,), w), u) for u in U]))
+    soft = torch.zeros(n, dtype=torch.int64, device=de.device)
+    mass = torch.zeros(n, dtype=torch.float64, device=de.device)
+    q, wmax = pack_fixed(de, soft, mass)
+    nib, nkb = (n + 127) // 128, (m + 31) // 32
+    t = q.cpu().numpy().reshape(nib, nkb, 128, 8, 16)
+    r = np.arange(128)[:, None]
+    unswz = t[:, :, r, (np.arange(8)[None, :] ^ (r % 8)), :]          # chunk order restored
+    lines = unswz.reshape(nib, nkb, 128, 4, 32).astype(np.uint64)       # [rb][kb][r][plane][cell]
+    qv = (lines[:, :, :, 0] << 24) | (lines[:, :, :, 1] << 16) | (lines[:, :, :, 2] << 8) | lines[:, :, :, 3]
+    qv = qv.transpose(0, 2, 1, 3).reshape(nib * 128, nkb * 32)
+    X = U.astype(np.float64)
+    A = X * (np.sqrt(w / w.max()) if weighted else 1.0)
+    want = np.rint(A * 2.0 ** 31).astype(np.uint64)
+    np.testing.assert_array_equal(qv[:n, :m], want)
+    assert not qv[n:].any() and not qv[:, m:].any()
+    np.testing.assert_array_equal(soft.cpu().numpy(), ((want & 0xFFFFFF) != 0).sum(1))
+    mh = (X * (w if weighted else 1.0)).sum(1)
+    np.testing.assert_allclose(mass.cpu().numpy(), mh, rtol=1e-13)
+    np.testing.assert_allclose(mass.cpu().numpy(), _masses_device(de).cpu().numpy(), rtol=1e-13)
+
+
 @pytest.mark.parametrize("n,m,weighted", [(3, 5, False), (5, 40, True), (129, 777, False),
                                           (300, 5000, True), (1100, 3000, False),
                                           (2200, 1500, False), (2200, 700, True)])
@@ -117,9 +151,9 @@ def test_fixed_gram_fused_sums(pb, n, m, weighted):
     ws = de.workspace(N.load().pidb_gram_fixed_workspace_bytes(n, de.m, 1))
 
     def run():
-        q, ldq, wmax = pack_fixed(de)
+        q, wmax = pack_fixed(de)
         rc = torch.zeros(2 * n, dtype=torch.float64, device=de.device)
-        _launch("pidb_gram_fixed_sums", q.data_ptr(), n, de.m, ldq, wmax, inv.data_ptr(),
+        _launch("pidb_gram_fixed_sums", q.data_ptr(), n, de.m, wmax, inv.data_ptr(),
                 rc.data_ptr(), rc.data_ptr() + 8 * n, ws.data_ptr(), ws.numel(),
                 torch.cuda.current_stream(de.device).cuda_stream)
         return rc.cpu().numpy()
