@@ -248,7 +248,29 @@ def disk_sample_cpu(res, n, seed=0):
     return out
 
 
-def cpu_reference(U, method, workers):
+def reference_module():
+    """The unmodified reference (baseline/_ref, tools/install_reference.sh) or None."""
+    from oracle import reference
+
+    try:
+        return reference.load()
+    except ImportError:
+        return None
+
+
+def cpu_reference(U, method, workers, dims=None):
+    """Seconds for one depth call of the CPU reference on host array U: the
+    real fuzzdepth (baseline/_ref) when installed, else oracle.port.  The
+    Ensemble (ProbMask validation) is built outside the timed call."""
+    fd = reference_module()
+    if fd is not None:
+        from oracle import reference
+
+        ens = reference.from_array(fd, U, dims)
+        fn = {"pid-mean": fd.depth_pid_mean, "eid": fd.depth_eid, "pid": fd.depth_pid}[method]
+        t0 = time.perf_counter()
+        fn(ens, workers=workers)
+        return time.perf_counter() - t0
     from oracle import port
 
     t0 = time.perf_counter()
@@ -261,6 +283,29 @@ def cpu_reference(U, method, workers):
     return time.perf_counter() - t0
 
 
+def cpu_kind():
+    return "reference" if reference_module() is not None else "port"
+
+
+def cpu_what():
+    fd = reference_module()
+    if fd is not None:
+        return (f"fuzzdepth {fd.__version__} (the unmodified reference, baseline/_ref; "
+                f"numpy {np.__version__}, OPENBLAS_NUM_THREADS="
+                f"{os.environ.get('OPENBLAS_NUM_THREADS', 'unset')})")
+    return "oracle.port (numpy/OpenBLAS restatement of fuzzdepth; baseline/_ref not installed)"
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_pair_baseline(U, method, n_full, m_full, what):
     """oracle.port on a bounded sample of an O(N^2 M) workload: measured
     pair-voxels/s plus the full-size time extrapolated from it (labelled)."""
@@ -268,9 +313,9 @@ def cpu_pair_baseline(U, method, n_full, m_full, what):
     sec = cpu_reference(U, method, workers)
     pv = U.shape[0] ** 2 * U.shape[1] / sec
     return {"value": U.shape[0] * U.shape[1] / sec, "unit": "member-voxels/s",
-            "pair_voxels_per_s": pv, "cores": workers, "kind": "port",
-            "sample": f"{U.shape[0]} members x {U.shape[1]} cells of {what}; oracle.port {method} "
-                      f"(numpy/OpenBLAS fp64 Gram tiles), ThreadPool({workers})",
+            "pair_voxels_per_s": pv, "cores": workers, "kind": cpu_kind(),
+            "sample": f"{U.shape[0]} members x {U.shape[1]} cells of {what}; {cpu_what()} "
+                      f"{method}, workers={workers}", "cpu_model": cpu_model(),
             "seconds": sec,
             "extrapolated_full_seconds": n_full ** 2 * m_full / pv,
             "extrapolation": "full-size time = N^2 M / measured pair-voxels/s (not measured)"}
@@ -280,11 +325,15 @@ def cpu_pair_baseline(U, method, n_full, m_full, what):
 
 
 def run_reference(args, rank, world):
+    """The reference's own CPU implementation on this box's host cores: the
+    unmodified fuzzdepth from baseline/_ref (oracle.port only when it is not
+    installed), each step one depth call on a bounded sample of the
+    workload (all members, the central planes), rank 0 only."""
     if rank != 0:
         return
     method, res, n, desc = WORKLOADS[args.workload]
     workers = os.cpu_count() or 1
-    planes = args.ref_planes or (8 if res >= 512 else max(1, res // 16))
+    planes = args.ref_planes or (REF_PLANES if res >= 512 else max(1, res // 16))
     if args.workload == "cfg1":  # the whole 2D ensemble (26 MB)
         U, planes = disk_sample_cpu(res, n), res
     else:
@@ -298,8 +347,8 @@ def run_reference(args, rank, world):
     sec = float(np.mean(ts))
     value = mv / sec
     sample = (f"{U.shape[0]} members x {planes} central planes of {res}^3 "
-              f"({U.shape[1]} cells/member) of the {args.workload} workload; oracle.port "
-              f"(numpy/OpenBLAS restatement of fuzzdepth {method}), ThreadPool({workers})")
+              f"({U.shape[1]} cells/member) of the {args.workload} workload; {cpu_what()} "
+              f"depth_{method.replace('-', '_')}(Ensemble of host ProbMasks), workers={workers}")
     line = {
         "impl": "reference", "metric": metric_name(method), "value": value,
         "unit": "member-voxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -307,11 +356,15 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "sample": sample},
         "cpu_baseline": {"value": value, "unit": "member-voxels/s", "cores": workers,
-                         "kind": "port", "sample": sample},
+                         "kind": cpu_kind(), "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "member-voxels/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# central planes of 512^3 in the CPU samples (reference arm, cpu_baseline)
+REF_PLANES = 16
 
 
 def ncu_traffic(workload, world):
@@ -409,9 +462,9 @@ def run_ours(args, rank, world, local, pg):
     if sampler is not None:
         line["clocks"] = sampler.summary()
 
-    # ---------------- CPU baseline (rank 0, N=1): oracle.port on a sample
+    # ---------------- CPU baseline (rank 0, N=1): the reference on a sample
     if rank == 0 and world == 1 and not args.no_cpu:
-        planes = args.ref_planes or (8 if res >= 512 else max(1, res // 16))
+        planes = args.ref_planes or (REF_PLANES if res >= 512 else max(1, res // 16))
         y0 = res // 2 - planes // 2
         lo, hi = y0 * res * res, (y0 + planes) * res * res
         if two_d:  # all of cfg1
@@ -423,12 +476,16 @@ def run_ours(args, rank, world, local, pg):
         sec = cpu_reference(U, method, workers)
         line["cpu_baseline"] = {
             "value": U.shape[0] * U.shape[1] / sec, "unit": "member-voxels/s", "cores": workers,
-            "kind": "port",
+            "kind": cpu_kind(), "cpu_model": cpu_model(),
             "sample": f"{U.shape[0]} members x {planes} central planes ({U.shape[1]} cells) "
-                      f"of the same ensemble; oracle.port {method} (fuzzdepth algorithm, "
-                      f"numpy/OpenBLAS), ThreadPool({workers}); PID-mean is GIL-bound "
-                      "(effectively 1 core) as in the reference",
+                      f"of the same ensemble (the same sample as the --impl reference arm); "
+                      f"{cpu_what()} depth_{method.replace('-', '_')}, workers={workers}; "
+                      "PID-mean is GIL-bound (effectively 1 core) in the reference",
         }
+
+    # ---------------- parity at full size against the CPU reference
+    if rank == 0 and world == 1 and not args.no_parity and args.workload == "cfg5":
+        line["parity"] = {"cfg5_pid_mean_full": parity_pid_mean_full(de, res_chk)}
 
     # ---------------- end to end from pinned host memory
     host = None
@@ -450,6 +507,63 @@ def run_ours(args, rank, world, local, pg):
 
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def _agreement(got, ref):
+    d = np.abs(np.asarray(got.depth) - np.asarray(ref.depth))
+    gap = float(np.min(np.diff(np.sort(ref.depth)))) if len(ref.depth) > 1 else None
+    return {"max_abs_depth_err": float(d.max()),
+            "max_abs_in_in_err": float(np.abs(got.in_in - ref.in_in).max()),
+            "max_abs_in_out_err": float(np.abs(got.in_out - ref.in_out).max()),
+            "rank_identical": bool(np.array_equal(np.asarray(got.rank), np.asarray(ref.rank))),
+            "rank_mismatches": int(np.sum(np.asarray(got.rank) != np.asarray(ref.rank))),
+            "ref_min_adjacent_gap": gap}
+
+
+def parity_pid_mean_full(de, got):
+    """Full-size depth_pid_mean of the REAL reference on the same device bytes
+    (lazy loaders copy one member at a time out of HBM) vs the GPU result."""
+    fd = reference_module()
+    if fd is None:
+        return {"skipped": "baseline/_ref not installed (tools/install_reference.sh)"}
+    from oracle import reference
+
+    workers = min(16, os.cpu_count() or 1)  # bounds host residency (one member per worker)
+    t0 = time.perf_counter()
+    ref = fd.depth_pid_mean(reference.lazy_from_device(fd, de), workers=workers)
+    out = {"reference": cpu_what(), "size": f"{de.n} x {de.m} cells (full config, "
+                                             f"{de.n * de.m:.3e} member-voxels)",
+           "reference_seconds": time.perf_counter() - t0, "workers": workers}
+    out.update(_agreement(got, ref))
+    return out
+
+
+def parity_pid_reduced(dev):
+    """cfg4 at reduced resolution (1000 x 64^3, SURVEY.md §7.3 hard part 4:
+    full-size CPU PID takes ~21 h): the real reference depth_pid vs the exact
+    GPU path and the tensor-core Gram path, on the same bytes."""
+    import paper_2512_15187_b200 as pb
+    from paper_2512_15187_b200 import depth as D
+    from paper_2512_15187_b200 import synth
+
+    fd = reference_module()
+    if fd is None:
+        return {"skipped": "baseline/_ref not installed (tools/install_reference.sh)"}
+    from oracle import reference
+
+    de = synth.ellipsoids_device(64, 1000, 0, 0, device=dev)
+    U = de.values[:, :de.m].cpu().numpy()
+    ens = reference.from_array(fd, U, de.dims, ids=list(de.ids))
+    t0 = time.perf_counter()
+    ref = fd.depth_pid(ens, workers=os.cpu_count() or 1)
+    sec = time.perf_counter() - t0
+    exact = pb.depth_pid(de, algorithm="factorized")
+    gram = pb.depth_pid(de, algorithm="gram")
+    cert = dict(D.LAST_GRAM_CERT)
+    return {"size": "1000 x 64^3 (cfg4 members and generator at reduced resolution)",
+            "reference": cpu_what(), "reference_seconds": sec,
+            "factorized_vs_reference": _agreement(exact, ref),
+            "gram_vs_reference": _agreement(gram, ref), "gram_certifier": cert}
 
 
 def prepare_e2e(de, world):
@@ -479,7 +593,7 @@ def run_e2e(args, host, _, meta, fn, world, pg, dev):
                                        cell_range=cr if world > 1 else None, device=dev)
         return fn(e)
 
-    ms = timed(step, max(1, min(args.steps, 3)), 1, world)
+    ms = timed(step, max(10, args.steps), 3, world)
     total = n * int(np.prod(dims))
     return {"value": total / (ms * 1e-3), "unit": "member-voxels/s", "ms_per_step": ms,
             "h2d_bytes_per_step": n * m * 4, "d2h_bytes_per_step": (5 * n + n + 1) * 8,
@@ -493,7 +607,10 @@ def run_e2e(args, host, _, meta, fn, world, pg, dev):
 # tools/probe_box.sh (8192^3, best of 20; profiles/r01_probe_box.log).
 TF32_TFLOPS_PROBE = 747.2
 READ_STREAM_PEAK_GBS = 7227.4  # TMA 2D read stream, 512-B rows (profiles/r01_ubench_tma.log)
-INT8_TOPS_PROBE = 3004.5
+# INT8 tensor peak: the higher of cuBLAS's int8 GEMM (3004.5 TOP/s) and our
+# tcgen05 kind::i8 issue-rate microbenchmark (tools/ubench_mma.cu, 128x128x32
+# MMAs, profiles/r02_ubench_mma.log: 4425 TOP/s); the roofline uses the max.
+INT8_TOPS_PROBE = 4425.0
 
 
 def run_pid_secondary(args, rank, world, pg, dev, pk):
@@ -542,7 +659,8 @@ def run_pid_secondary(args, rank, world, pg, dev, pk):
                                        "exact int32 accumulation, fused PID sums)",
                              "achieved": ach, "unit": "TFLOP/s", "peak": mode_peak,
                              "frac": ach / mode_peak,
-                             "peak_src": "cuBLAS INT8 probe / 10 (10 digit-pair MMAs per product)",
+                             "peak_src": "INT8 tensor peak (tcgen05 microbenchmark, 4425 TOP/s) / 10 "
+                                         "(10 digit-pair MMAs per product)",
                              "frac_vs_tf32x3": ach / (TF32_TFLOPS_PROBE / 3),
                              "executed_int8_ops": executed,
                              "executed_frac_of_int8_peak": executed / (kg * 1e-3) / 1e12 / INT8_TOPS_PROBE,
@@ -556,6 +674,8 @@ def run_pid_secondary(args, rank, world, pg, dev, pk):
             "max_rel_depth_err": float(np.abs(a.depth - b.depth).max() / np.abs(b.depth).max()),
             "rank_mismatches": int(np.sum(a.rank != b.rank)),
             "min_depth_gap": float(np.min(np.diff(np.sort(b.depth))))}
+    if rank == 0 and world == 1 and not args.no_parity:
+        out["parity_1000x64"] = parity_pid_reduced(dev)
     out["ms_per_depth"] = out["factorized"]["ms_per_depth"]
     out["value"] = out["factorized"]["value"]
     out["algorithm"] = "factorized (exact, default)"
@@ -607,7 +727,7 @@ def run_eid_secondary(args, dev, pk):
                              "achieved": ops / (kg * 1e-3) / 1e12, "unit": "TOP/s",
                              "peak": INT8_TOPS_PROBE, "frac": ops / (kg * 1e-3) / 1e12 / INT8_TOPS_PROBE,
                              "kernel_ms": kg, "algorithmic_ops": ops,
-                             "peak_src": "cuBLAS INT8 probe (torch._int_mm 8192^3)"},
+                             "peak_src": "INT8 tensor peak (tcgen05 microbenchmark, profiles/r02_ubench_mma.log)"},
            "masses_ms": km,
            "ms_per_depth_graph": ms_graph}
     if cpu is not None:
@@ -628,6 +748,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pid", action="store_true")
     ap.add_argument("--no-eid", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--ref-planes", type=int, default=0)
     ap.add_argument("--ref-pid-members", type=int, default=64)
     args = ap.parse_args()
