@@ -228,6 +228,10 @@ int pidb_copy_rows(void* dst, int64_t dst_pitch_bytes, const void* src,
                    int64_t src_pitch_bytes, int64_t row_bytes, int64_t rows,
                    void* stream);
 
+/* dst[j] = sum_k src[k*len + j] for k = 0..rows-1 in ascending order: the
+ * fixed-order combination of per-slab partial sums (streamed PID-mean). */
+int pidb_sum_rows(const double* src, int64_t rows, int64_t len, double* dst, void* stream);
+
 /* One-pass value check of raw member data (ProbMask policy, grid.py:105-116):
  * stats (device, 3 x 8 bytes) = {#non-finite, min key, max key} where the
  * keys are order-preserving int64 images of the doubles; clamp != 0 clips

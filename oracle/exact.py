@@ -72,14 +72,17 @@ def ranks(depth):
     return np.array(r, dtype=np.int64)
 
 
-def intersections(B: np.ndarray) -> np.ndarray:
-    """Exact |C_i ∩ C_j| for 0/1 rows: float64 BLAS on 0/1 values is exact
-    while every count stays below 2^53."""
-    X = np.asarray(B, dtype=np.float64)
-    if X.shape[1] >= 2**53:
-        raise ValueError("too many cells for exact float64 counts")
-    G = X @ X.T
-    return np.rint(G).astype(np.int64)
+def intersections(B: np.ndarray, chunk: int = 1 << 24) -> np.ndarray:
+    """Exact |C_i ∩ C_j| for 0/1 rows: float32 BLAS over column chunks of at
+    most 2^24 cells is exact (0/1 products, partial counts < 2^24), and the
+    chunk counts are summed as int64."""
+    B = np.asarray(B)
+    n, m = B.shape
+    I = np.zeros((n, n), dtype=np.int64)
+    for lo in range(0, m, chunk):
+        X = np.asarray(B[:, lo:lo + chunk], dtype=np.float32)
+        I += np.rint(X @ X.T).astype(np.int64)
+    return I
 
 
 def eid_fast(B: np.ndarray):

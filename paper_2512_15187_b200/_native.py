@@ -76,6 +76,7 @@ SIGNATURES: dict[str, tuple] = {
     "pidb_mean_mask": (_int, [_p, _int, _i64, _i64, _i64, _p, _p]),
     "pidb_copy_rows": (_int, [_p, _i64, _p, _i64, _i64, _i64, _p]),
     "pidb_validate": (_int, [_p, _int, _i64, _i64, _i64, _int, _p, _p]),
+    "pidb_sum_rows": (_int, [_p, _i64, _i64, _p, _p]),
     "pidb_synth_ellipsoids": (_int, [_p, _i64, _i64, _i64, _p, _dbl, _p]),
     "pidb_synth_disks": (_int, [_p, _i64, _i64, _i64, _p, _dbl, _p]),
     "pidb_band_envelopes": (_int, [_p, _int, _i64, _i64, _i64, _p, _i64, _dbl, _p, _int, _p, _p,

@@ -374,8 +374,33 @@ __global__ void validate_f32x4_kernel(float* __restrict__ u, int64_t n, int64_t 
   }
   validate_reduce(bad, (double)lo, (double)hi, any, nonfinite, kmin, kmax);
 }
+__global__ void validate_init_kernel(unsigned long long* nf, long long* kmin, long long* kmax) {
+  *nf = 0;
+  *kmin = 0x7FFFFFFFFFFFFFFFLL;
+  *kmax = (long long)0x8000000000000000ULL;
+}
+
+// dst[j] = sum_k src[k * len + j], k ascending (fixed order).
+__global__ void sum_rows_kernel(const double* __restrict__ src, int64_t rows, int64_t len,
+                                double* __restrict__ dst) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < len;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t k = 0; k < rows; ++k) s += src[k * len + j];
+    dst[j] = s;
+  }
+}
 }  // namespace
 }  // namespace pidb
+
+extern "C" int pidb_sum_rows(const double* src, int64_t rows, int64_t len, double* dst,
+                             void* stream) {
+  PIDB_REQUIRE(src && dst && rows >= 1 && len >= 1, "bad arguments to pidb_sum_rows");
+  const int blocks = (int)std::min<int64_t>((len + 255) / 256, 148 * 4);
+  sum_rows_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(src, rows, len, dst);
+  PIDB_LAUNCH_CHECK("sum_rows_kernel");
+  return PIDB_OK;
+}
 
 extern "C" int pidb_validate(void* u, int dtype, int64_t n, int64_t m, int64_t ld, int clamp,
                              void* stats, void* stream) {
@@ -384,8 +409,8 @@ extern "C" int pidb_validate(void* u, int dtype, int64_t n, int64_t m, int64_t l
   unsigned long long* nf = static_cast<unsigned long long*>(stats);
   long long* kmin = reinterpret_cast<long long*>(nf + 1);
   long long* kmax = kmin + 1;
-  const long long init[3] = {0, 0x7FFFFFFFFFFFFFFFLL, (long long)0x8000000000000000ULL};
-  PIDB_CUDA(cudaMemcpyAsync(stats, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  validate_init_kernel<<<1, 1, 0, st>>>(nf, kmin, kmax);  // capturable (no host memcpy)
+  PIDB_LAUNCH_CHECK("validate_init_kernel");
   const dim3 blocks((unsigned)std::min<int64_t>((m + 255) / 256, 64),
                     (unsigned)std::min<int64_t>(n, 1024));
   if (dtype == PIDB_F32 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(u) & 15) == 0) {

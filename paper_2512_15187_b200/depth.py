@@ -322,6 +322,8 @@ def depth_pid_mean(ensemble, workers: int | None = None,
     """
     t0 = time.perf_counter()
     resolve_workers(workers)
+    if _streamable(ensemble):
+        return _pid_mean_streamed(ensemble, t0, cv_warn_threshold)
     de = stage(ensemble)
     n, dev = de.n, de.device
 
@@ -346,6 +348,103 @@ def depth_pid_mean(ensemble, workers: int | None = None,
             "pid-mean ranks may diverge from exact pid",
             RuntimeWarning,
             stacklevel=2,
+        )
+    return res
+
+
+# Host-resident inputs larger than this stream through HBM in cell slabs.
+STREAM_SLAB_BYTES = int(os.environ.get("PIDB_STREAM_SLAB_BYTES", str(2 << 30)))
+
+
+def _streamable(x) -> bool:
+    return (isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.dim() >= 2
+            and x.dtype in (torch.float32, torch.float64) and x.shape[0] >= 1
+            and x.numel() * x.element_size() > 2 * STREAM_SLAB_BYTES)
+
+
+def _pid_mean_streamed(host: torch.Tensor, t0: float, cv_warn_threshold: float) -> DepthResult:
+    """PID-mean of a pinned host ensemble without staging it whole: cell slabs
+    (every member, a range of cells) are copied on a side stream into two
+    HBM slab buffers while the previous slab is validated in place
+    (ProbMask policy, grid.py:105-116) and swept by K5 on the compute
+    stream; the per-slab partial sums are additive over cells (the same
+    decomposition as the multi-GPU voxel shards) and are combined in slab
+    order, then the K4 epilogue runs once.  HBM holds two slabs, not the
+    ensemble; copies, validation and K5 overlap."""
+    from .device import _key_to_double, require_cuda
+    from .grid import VALUE_TOLERANCE
+
+    dev = require_cuda()
+    n = int(host.shape[0])
+    flat = host.reshape(n, -1)
+    if flat.stride(1) != 1:
+        raise ValidationError("host member tensor must have contiguous rows")
+    m = int(flat.shape[1])
+    es = flat.element_size()
+    dt = flat.dtype
+    code = N.PIDB_F64 if dt == torch.float64 else N.PIDB_F32
+    S = max(32, (STREAM_SLAB_BYTES // (n * es)) // 32 * 32)
+    S = min(S, (m + 31) // 32 * 32)
+    slabs = [(c0, min(m, c0 + S)) for c0 in range(0, m, S)]
+    K = torch.cuda.current_stream(dev)
+    C = torch.cuda.Stream(dev)
+    bufs = [torch.empty((n, S), dtype=dt, device=dev) for _ in range(2)]
+    part = torch.empty((len(slabs), 2 * n + 1), dtype=torch.float64, device=dev)
+    stats = torch.empty((len(slabs), 3), dtype=torch.int64, device=dev)
+    lib = N.load()
+    ws = torch.zeros(max(1, lib.pidb_pid_mean_workspace_bytes(n, S, code)), dtype=torch.uint8,
+                     device=dev)
+    free = [None, None]
+    src0 = flat.data_ptr()
+    for k, (c0, c1) in enumerate(slabs):
+        b = k & 1
+        buf = bufs[b]
+        if free[b] is not None:
+            C.wait_event(free[b])
+        N.call("pidb_copy_rows", buf.data_ptr(), S * es, src0 + c0 * es, flat.stride(0) * es,
+               (c1 - c0) * es, n, C.cuda_stream)
+        landed = torch.cuda.Event()
+        landed.record(C)
+        K.wait_event(landed)
+        mk = c1 - c0
+        N.call("pidb_validate", buf.data_ptr(), code, n, mk, S, 1, stats[k].data_ptr(),
+               K.cuda_stream)
+        p = part[k].data_ptr()
+        _launch("pidb_pid_mean_partials", buf.data_ptr(), code, n, mk, S, None, p, p + 8 * n,
+                p + 16 * n, ws.data_ptr(), ws.numel(), K.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(K)
+        free[b] = ev
+    out = _Out(n, dev, extra=2 * n + 1)
+    N.call("pidb_sum_rows", part.data_ptr(), len(slabs), 2 * n + 1, out.extra.data_ptr(),
+           K.cuda_stream)
+    pe = out.extra.data_ptr()
+    inv, ii, io, d = out.ptrs()
+    N.call("pidb_depth_epilogue", N.PIDB_EPI_PID_MEAN, n, pe, pe + 8 * n, pe + 16 * n,
+           inv, ii, io, d, out.rank.data_ptr(), K.cuda_stream)
+    st = stats.cpu().numpy()
+    out.host()
+    if st[:, 0].any():
+        raise ValidationError("mask values must be finite")
+    lo, hi = _key_to_double(int(st[:, 1].min())), _key_to_double(int(st[:, 2].max()))
+    if lo < -VALUE_TOLERANCE or hi > 1.0 + VALUE_TOLERANCE:
+        raise ValidationError(f"mask values outside [0, 1]: min={lo!r} max={hi!r}")
+    host_ex = out.host_extra()[n:]
+    masses, col_mean = host_ex[:n], float(host_ex[n])
+    if col_mean == 0.0:
+        raise DegenerateEnsembleError("ensemble mean mask is identically zero")
+    in_in, in_out, depth, rank = out.fetch()
+    from .device import _make_ids
+
+    res = DepthResult(ids=_make_ids(None, n), in_in=in_in, in_out=in_out, depth=depth,
+                      rank=rank, method="pid-mean", cv_mass=mass_cv(masses),
+                      elapsed_seconds=time.perf_counter() - t0)
+    if res.cv_mass > cv_warn_threshold:
+        warnings.warn(
+            f"member mass CV {res.cv_mass:.3g} exceeds {cv_warn_threshold:g}; "
+            "pid-mean ranks may diverge from exact pid",
+            RuntimeWarning,
+            stacklevel=3,
         )
     return res
 
@@ -477,6 +576,10 @@ def _pid_gram(de: DeviceEnsemble, out: _Out) -> np.ndarray:
         blk[4 * n:5 * n] = ranks_from_depths(blk[3 * n:4 * n]).view(np.float64)
         out._host = blk
     return masses
+
+
+def _gram_available() -> bool:
+    return N.has_symbol("pidb_gram_fixed_sums")
 
 
 def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") -> DepthResult:

@@ -825,3 +825,34 @@ def test_validate_kernel_stats(pb, n, m, ld, clamp):
         fmask = np.isfinite(w)
         w[fmask] = np.clip(w[fmask], 0.0, 1.0)
     np.testing.assert_array_equal(got, want)
+
+
+def test_pid_mean_streamed_from_pinned_host(pb, monkeypatch):
+    """depth_pid_mean on a pinned host tensor larger than two slabs streams
+    through HBM in cell slabs (H2D / validation / K5 overlapped, partials
+    combined in slab order): same depths as the resident path (1e-13) and
+    the oracle, identical ranks; ragged last slab; the ProbMask policy
+    (clamp within tolerance, errors outside) still applies."""
+    from paper_2512_15187_b200 import depth as D
+
+    monkeypatch.setattr(D, "STREAM_SLAB_BYTES", 1 << 20)
+    rng = np.random.default_rng(31)
+    U = rng.uniform(size=(37, 60001)).astype(np.float32)
+    U[3, 5] = 1.0 + 5e-10  # clamped like ProbMask
+    host = torch.from_numpy(U).pin_memory()
+    assert D._streamable(host)
+    got = pb.depth_pid_mean(host)
+    Uc = np.clip(U, 0.0, 1.0)
+    want = port.depth_pid_mean(Uc)
+    close(got.depth, want["depth"], 1e-13)
+    close(got.in_in, want["in_in"], 1e-13)
+    np.testing.assert_array_equal(got.rank, want["rank"])
+    resident = pb.depth_pid_mean(torch.from_numpy(Uc))
+    close(got.depth, resident.depth, 1e-13)
+    bad = host.clone().pin_memory()
+    bad[7, 59999] = 1.5
+    with pytest.raises(pb.ValidationError):
+        pb.depth_pid_mean(bad)
+    bad[7, 59999] = float("nan")
+    with pytest.raises(pb.ValidationError):
+        pb.depth_pid_mean(bad)
