@@ -123,6 +123,19 @@ size_t pidb_gram_i8_workspace_bytes(int64_t n, int64_t m);
 int pidb_gram_i8(const uint8_t* b, int64_t n, int64_t m, int64_t ldb,
                  int64_t* gram, void* ws, size_t ws_bytes, void* stream);
 
+/* K7 + K2 in one launch (eID, unit weights): the CTAs of each K split pack
+ * that split's cells to u8 (into b, (n, ldb), ldb % 128 == 0, 128-byte
+ * aligned) chunk by chunk and count non-binary values (nonbinary, zero-
+ * filled by the caller), while the tensor cores consume the chunks already
+ * published; then the same exact int64 Gram as pidb_gram_i8.  Needs one
+ * wave of CTAs: returns PIDB_EUNSUPPORTED otherwise (use pidb_binary_pack +
+ * pidb_gram_i8).  Workspace: pidb_eid_gram_fused_workspace_bytes, zero-
+ * filled once (its split counters return to zero). */
+size_t pidb_eid_gram_fused_workspace_bytes(int64_t n, int64_t m);
+int pidb_eid_gram_fused(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
+                        uint8_t* b, int64_t ldb, int64_t* nonbinary, int64_t* gram,
+                        void* ws, size_t ws_bytes, void* stream);
+
 /* --------------------------------------------------------------- K1x ----
  * Fixed-point Gram on the int8 tensor cores with exact integer accumulation
  * (the tensor-core formulation of _pairwise_sums/gram_block for PID,

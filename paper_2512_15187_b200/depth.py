@@ -614,6 +614,40 @@ def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") 
     return _finish(de, out, "pid", masses, t0)
 
 
+_FUSED_EID = os.environ.get("PIDB_EID_FUSED", "1") != "0"  # A/B hook
+
+
+def _eid_gram_fused(de: DeviceEnsemble, nb: torch.Tensor):
+    """K7 + K2 in one launch (pidb_eid_gram_fused); None when the shape needs
+    more than one wave of CTAs (then pack and Gram run as two kernels)."""
+    if not _FUSED_EID:
+        return None
+    lib = N.load()
+    ldb = (de.m + 127) // 128 * 128
+    key = ("eid_u8", ldb)
+    b = de._cache.get(key)
+    if b is None or torch.cuda.is_current_stream_capturing():
+        b = torch.empty((de.n, ldb), dtype=torch.uint8, device=de.device)
+        if not torch.cuda.is_current_stream_capturing():
+            de._cache[key] = b
+    g = torch.empty((de.n, de.n), dtype=torch.int64, device=de.device)
+    ws = de.workspace(lib.pidb_eid_gram_fused_workspace_bytes(de.n, de.m))
+    ev = None
+    if KERNEL_EVENTS is not None:
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
+    rc = lib.pidb_eid_gram_fused(de.ptr(), de.dtype_code, de.n, de.m, de.ld, b.data_ptr(), ldb,
+                                 nb.data_ptr(), g.data_ptr(), ws.data_ptr(), ws.numel(),
+                                 stream_ptr(de.device))
+    if rc == N.PIDB_EUNSUPPORTED:
+        return None
+    N.check(rc, "pidb_eid_gram_fused")
+    if ev is not None:
+        ev[1].record()
+        KERNEL_EVENTS.append(("pidb_eid_gram_fused", *ev))
+    return g
+
+
 def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
     """Inclusion depth of binary ensembles (depth.py:192-210).
 
@@ -631,13 +665,19 @@ def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
         def enqueue():
             # K7 packs and counts non-binary values in the same pass (the
             # counts ride in the result block); the masses are the Gram
-            # diagonal |C_i| (exact integers)
+            # diagonal |C_i| (exact integers).  One wave fits: K7 fused into
+            # the K2 launch (pack and Gram overlap), else the two kernels.
             out = _Out(n, dev, extra=n)
             nb = out.extra.view(torch.int64)
             nb.zero_()
-            packed = pack_binary(de, nb)
-            _allreduce(nb, de)
-            g = intersection_gram(de, packed)
+            g = _eid_gram_fused(de, nb)
+            if g is None:
+                packed = pack_binary(de, nb)
+                _allreduce(nb, de)
+                g = intersection_gram(de, packed)
+            else:
+                _allreduce(nb, de)
+                _allreduce(g, de)
             mslot, ii, io, d = out.ptrs()
             N.call("pidb_eid_exact_epilogue", g.data_ptr(), n, ii, io, d, out.rank.data_ptr(),
                    mslot, stream_ptr(dev))
