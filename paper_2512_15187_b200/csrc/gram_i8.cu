@@ -171,9 +171,10 @@ __global__ void gram_i8_reduce_kernel(const int32_t* __restrict__ part, int n, i
 // packed just before (L2-hot), so the pack and the Gram overlap instead of
 // running back to back.  Needs every CTA resident (one wave); the
 // workspace's split counters return to zero at exit.
-constexpr int kPackWarps = 8;
-constexpr int kFusedThreads = (6 + kPackWarps) * 32;  // 0 TMA, 1 MMA, 2-5 epilogue, 6-13 pack
-constexpr int kChunkBlocks = 8;                       // K blocks (128 cells) per published chunk
+constexpr int kPackWarps = 16;
+constexpr int kPackUnroll = 2;                        // segments in flight per packer lane
+constexpr int kFusedThreads = (6 + kPackWarps) * 32;  // 0 TMA, 1 MMA, 2-5 epilogue, 6-21 pack
+constexpr int kChunkBlocks = 32;                       // K blocks (128 cells) per published chunk
 
 struct FusedParams {
   GramI8Params g;
@@ -186,11 +187,11 @@ struct FusedParams {
   unsigned* done;   // [splits] CTAs finished
 };
 
+// 16 cells per lane: 16-byte loads when the span is whole (load and pack
+// phases are split so a lane keeps several segments in flight)
 template <typename T>
-__device__ __forceinline__ void pack_segment(const T* __restrict__ row, int64_t x0, int64_t xend,
-                                             uint8_t* __restrict__ dst, unsigned long long& bad) {
-  // 16 cells per lane: 16-byte loads when the span is whole
-  T vals[16];
+__device__ __forceinline__ void load_segment(const T* __restrict__ row, int64_t x0, int64_t xend,
+                                             T (&vals)[16]) {
   if (x0 + 16 <= xend) {
     constexpr int PER = 16 / sizeof(T);
 #pragma unroll
@@ -204,14 +205,22 @@ __device__ __forceinline__ void pack_segment(const T* __restrict__ row, int64_t 
 #pragma unroll
     for (int e = 0; e < 16; ++e) vals[e] = x0 + e < xend ? row[x0 + e] : T(0);
   }
+}
+
+template <typename T>
+__device__ __forceinline__ unsigned store_segment(const T (&vals)[16], int64_t x0, int64_t xend,
+                                                  uint8_t* __restrict__ dst) {
   uint32_t packed[4] = {0, 0, 0, 0};
+  unsigned bad = 0;
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     const T v = vals[e];
     bad += (x0 + e < xend) && !(v == T(0) || v == T(1));
     packed[e >> 2] |= (uint32_t)(v != T(0)) << (8 * (e & 3));
   }
-  if (x0 < xend) *reinterpret_cast<uint4*>(dst + x0) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+  if (x0 < xend)
+    *reinterpret_cast<uint4*>(dst + x0) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+  return bad;
 }
 
 template <typename T>
@@ -261,17 +270,40 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const int64_t xa = (int64_t)(kb0 + c * kChunkBlocks) * kBK;
       const int64_t xb = min(p.m, (int64_t)min(kb1, kb0 + (c + 1) * kChunkBlocks) * kBK);
       const int64_t segs = (xb - xa + 511) / 512;
-      for (int64_t job = pw; job < (int64_t)(r1 - r0) * segs; job += kPackWarps) {
-        const int64_t r = r0 + job / segs;
-        const int64_t x0 = xa + (job % segs) * 512 + lane * 16;
-        unsigned long long bad = 0;
-        pack_segment(u + r * p.ld, x0, xb, p.b + r * p.ldb, bad);
-        bad = __reduce_add_sync(0xffffffffu, (unsigned)bad);
-        if (lane == 0 && bad && p.nonbinary) atomicAdd(p.nonbinary + r, bad);
+      const int64_t jobs = (int64_t)(r1 - r0) * segs;
+      constexpr int U = sizeof(T) == 4 ? kPackUnroll : 1;  // fp64: register budget
+      for (int64_t j0 = pw; j0 < jobs; j0 += kPackWarps * U) {
+        T vals[U][16];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int64_t job = j0 + q * kPackWarps;
+          if (job < jobs) {
+            const int64_t r = r0 + job / segs;
+            load_segment(u + r * p.ld, xa + (job % segs) * 512 + lane * 16, xb, vals[q]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int64_t job = j0 + q * kPackWarps;
+          if (job < jobs) {
+            const int64_t r = r0 + job / segs;
+            unsigned bad =
+                store_segment(vals[q], xa + (job % segs) * 512 + lane * 16, xb, p.b + r * p.ldb);
+            bad = __reduce_add_sync(0xffffffffu, bad);
+            if (lane == 0 && bad && p.nonbinary) atomicAdd(p.nonbinary + r, (unsigned long long)bad);
+          }
+        }
       }
       __threadfence();
       asm volatile("bar.sync 2, %0;" ::"n"(kPackWarps * 32) : "memory");
-      if (pw == 0 && lane == 0) atomicAdd(p.ready + split, 1u);  // release (after the fences)
+      if (pw == 0 && lane == 0) {
+        // publish chunk c only once every CTA of the split published c - 1:
+        // the counter then reaches (c + 1) * ntiles exactly when chunk c is
+        // complete everywhere (no CTA can count ahead of a straggler)
+        const unsigned prior = (unsigned)c * (unsigned)g.ntiles;
+        while (ld_acquire_gpu(p.ready + split) < prior) __nanosleep(32);
+        atomicAdd(p.ready + split, 1u);  // release (after the fences)
+      }
     }
   } else if (warp == 0) {
     if (tc::elect_one()) {

@@ -614,7 +614,11 @@ def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") 
     return _finish(de, out, "pid", masses, t0)
 
 
-_FUSED_EID = os.environ.get("PIDB_EID_FUSED", "1") != "0"  # A/B hook
+# K7 fused into the K2 launch: correct (tests/test_gpu_parity.py) but measured
+# slower at cfg2 than the two kernels (0.178 vs 0.168 ms: 16 packer warps per
+# SM stream the members at ~3 TB/s, the standalone pack at ~6.8 TB/s;
+# profiles/r02_eid_fused_ab.log), so it is opt-in: PIDB_EID_FUSED=1.
+_FUSED_EID = os.environ.get("PIDB_EID_FUSED", "0") == "1"
 
 
 def _eid_gram_fused(de: DeviceEnsemble, nb: torch.Tensor):

@@ -867,6 +867,7 @@ def test_eid_fused_pack_gram(pb, monkeypatch, n, m, f64):
     calls (counters back at zero) agree."""
     from paper_2512_15187_b200 import depth as D
 
+    monkeypatch.setattr(D, "_FUSED_EID", True)
     rng = np.random.default_rng(n + m)
     B = (rng.uniform(size=(n, m)) < 0.45).astype(np.float64 if f64 else np.float32)
     de = pb.DeviceEnsemble.from_tensor(torch.from_numpy(B))
