@@ -369,12 +369,12 @@ REF_PLANES = 16
 
 def ncu_traffic(workload, world):
     """DRAM bytes (read + write) per K5 launch from the committed ncu capture of
-    the same workload (profiles/r01_traffic.json), or None."""
+    the same workload (profiles/r02_traffic.json), or None."""
     if world != 1:
         return None
     try:
         with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                               "r01_traffic.json")) as fh:
+                               "r02_traffic.json")) as fh:
             t = json.load(fh).get(workload)
         return None if t is None else t["dram_read_bytes"] + t["dram_write_bytes"]
     except (OSError, ValueError, KeyError):
@@ -677,7 +677,10 @@ def run_pid_secondary(args, rank, world, pg, dev, pk):
                              "frac_vs_tf32x3": ach / (TF32_TFLOPS_PROBE / 3),
                              "executed_int8_ops": executed,
                              "executed_frac_of_int8_peak": executed / (kg * 1e-3) / 1e12 / INT8_TOPS_PROBE,
-                             "kernel_ms": kg, "pack_ms": kp, "algorithmic_flops": flops}
+                             "kernel_ms": kg, "pack_ms": kp, "algorithmic_flops": flops,
+                             "traffic": ncu_traffic("cfg4_gram", world),
+                             "traffic_note": "ncu DRAM read+write bytes of one K1x launch at cfg4 "
+                                             "(profiles/r02_traffic.json): 1.7x the unique digit bytes"}
             o["certifier"] = dict(D.LAST_GRAM_CERT)
         out[alg] = o
     if len(results) == 2:

@@ -167,24 +167,44 @@ __global__ void __launch_bounds__(256, 3)
 #pragma unroll
       for (int j = 0; j < kPackIter / 4; ++j) {
         const int64_t x = (b + 4 * j + sub) * kCellsPerStage + 4 * wi;
-        uint32_t d[4] = {0u, 0u, 0u, 0u};  // plane words: byte e = digit of cell x + e
+        uint32_t qv[4];
+        if constexpr (sizeof(T) == 4) {
+          if (!w) {
+            // unweighted fp32: u 2^31 is exact in fp32, so is its rounding
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          double a = v[j][e];
-          if (w && x + e < m) {
-            const double wx = __ldcs(w + x + e);
-            mass = fma(wx, a, mass);
-            a *= sqrt(wx * inv_wmax);
-          } else {
-            mass += a;
+            for (int e = 0; e < 4; ++e) {
+              const float f = (float)v[j][e];
+              mass += (double)f;
+              qv[e] = min(__float2uint_rn(f * 2147483648.0f), 0x80000000u);
+            }
           }
-          const uint32_t qq = fx_quant(a);
-          cnt += (qq & 0xFFFFFFu) != 0u;
-          d[0] |= (qq >> 24) << (8 * e);
-          d[1] |= ((qq >> 16) & 255u) << (8 * e);
-          d[2] |= ((qq >> 8) & 255u) << (8 * e);
-          d[3] |= (qq & 255u) << (8 * e);
         }
+        if (sizeof(T) != 4 || w) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            double a = v[j][e];
+            if (w && x + e < m) {
+              const double wx = __ldcs(w + x + e);
+              mass = fma(wx, a, mass);
+              a *= sqrt(wx * inv_wmax);
+            } else {
+              mass += a;
+            }
+            qv[e] = fx_quant(a);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cnt += (qv[e] & 0xFFFFFFu) != 0u;
+        // 4 x 4 byte transpose: plane word k = byte (3 - k) of q0..q3
+        const uint32_t lo01 = __byte_perm(qv[0], qv[1], 0x5140);  // q0.b0 q1.b0 q0.b1 q1.b1
+        const uint32_t hi01 = __byte_perm(qv[0], qv[1], 0x7362);  // q0.b2 q1.b2 q0.b3 q1.b3
+        const uint32_t lo23 = __byte_perm(qv[2], qv[3], 0x5140);
+        const uint32_t hi23 = __byte_perm(qv[2], qv[3], 0x7362);
+        uint32_t d[4];
+        d[0] = __byte_perm(hi01, hi23, 0x7632);  // digit 0 = byte 3 (most significant)
+        d[1] = __byte_perm(hi01, hi23, 0x5410);
+        d[2] = __byte_perm(lo01, lo23, 0x7632);
+        d[3] = __byte_perm(lo01, lo23, 0x5410);
         // line r = r8 + warp: byte 32k + 4wi -> chunk (2k + wi/4) ^ (r % 8) = ^ warp
 #pragma unroll
         for (int k = 0; k < 4; ++k)
