@@ -1,8 +1,11 @@
 """Randomised parity sweep of every streaming-kernel variant against the CPU
 oracle: python tools/fuzz_parity.py SECONDS [seed]
 (n log-uniform in 1..6000, cells log-uniform, fp32/fp64, weighted or not,
-PID-mean / PID / dice / IoU / masses, and binary eID; depths within 1e-11,
-ranks equal wherever the oracle's depth gaps exceed 1e-11)."""
+PID-mean / PID / dice / IoU / masses, binary eID, and -- round 2 -- the
+tensor-core PID (K1x + certifier: depths within 1e-8, ranks equal), the
+fp64 gram_block seam (rtol 1e-12) and, for pinned host inputs, the streamed
+PID-mean; depths within 1e-11, ranks equal wherever the oracle's depth gaps
+exceed 1e-11)."""
 import sys
 import time
 import warnings
@@ -50,7 +53,36 @@ while time.time() < t_end:
                 checks.append((meas, pb.depth_similarity_baseline(de, meas),
                                port.depth_similarity(U, meas, w, workers=8)))
         if n * n * m <= 4e10:
-            checks.append(("pid", pb.depth_pid(de), port.depth_pid(U, w, workers=8)))
+            ref_pid = port.depth_pid(U, w, workers=8)
+            checks.append(("pid", pb.depth_pid(de), ref_pid))
+            if U.sum() > 0 and n <= 3000:
+                g = pb.depth_pid(de, algorithm="gram")
+                gerr = float(np.max(np.abs(g.depth - ref_pid["depth"])))
+                if gerr > 1e-8 or not ranks_ok(g.rank, ref_pid["depth"], ref_pid["rank"]):
+                    print(f"FAIL pid-gram n={n} m={m} f64={f64} w={weighted} err={gerr:.2e}",
+                          flush=True)
+                    fails += 1
+        if rng.uniform() < 0.1 and n * m <= 4e6:
+            from paper_2512_15187_b200.reduction import gram_block
+
+            k = max(1, n // 2)
+            got = gram_block(U[:k], U[k:] if n > 1 else U, w, complement_cols=binary)
+            A = U[:k].astype(np.float64) * (1.0 if w is None else w)
+            B = (U[k:] if n > 1 else U).astype(np.float64)
+            want = A @ (1.0 - B if binary else B).T
+            if not np.allclose(got, want, rtol=1e-12, atol=1e-300):
+                print(f"FAIL gram_block n={n} m={m} f64={f64} w={weighted}", flush=True)
+                fails += 1
+        if not weighted and U.sum() > 0 and rng.uniform() < 0.15 and n * m * U.itemsize > 1 << 16:
+            from paper_2512_15187_b200 import depth as D
+
+            old = D.STREAM_SLAB_BYTES
+            D.STREAM_SLAB_BYTES = max(4096, n * m * U.itemsize // int(rng.integers(3, 9)))
+            try:
+                r = pb.depth_pid_mean(torch.from_numpy(U).pin_memory())
+            finally:
+                D.STREAM_SLAB_BYTES = old
+            checks.append(("pid-mean-streamed", r, port.depth_pid_mean(U, w, workers=8)))
         mass = pb.member_masses(de)
         ok = np.allclose(mass, port.masses(U, w), rtol=1e-12, atol=1e-9)
         if not ok:
