@@ -108,33 +108,26 @@ int pidb_member_masses(const void* u, int dtype, int64_t n, int64_t m,
                        void* stream);
 
 /* ---------------------------------------------------------------- K7 ----
- * Pack 0/1 members to uint8 rows (ldb bytes, multiple of 16, zero padded up
- * to ldb) for the integer Gram.  Values other than 0/1 are counted in
- * nonbinary[i] (may be NULL) and packed as (u != 0). */
+ * Pack 0/1 members to u8 tiles for the integer Gram: 16 KB per (128
+ * members, 128 cells), laid out [row block][cell block] in the 128-byte-
+ * swizzled K-major order tcgen05 reads (line i % 128, 16-byte chunk c at
+ * c ^ (i % 8)); pidb_binary_pack_bytes(n, m) bytes, 1 KB aligned, ZERO-
+ * FILLED once by the caller (member rows past n, up to a multiple of 256,
+ * stay zero).  Values other than 0/1 are counted in nonbinary[i] (may be
+ * NULL, zero-filled by the caller) and packed as (u != 0). */
+size_t pidb_binary_pack_bytes(int64_t n, int64_t m);
 int pidb_binary_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
-                     uint8_t* b, int64_t ldb, int64_t* nonbinary, void* stream);
+                     uint8_t* tiles, int64_t* nonbinary, void* stream);
 
 /* ---------------------------------------------------------------- K2 ----
  * Exact integer intersection Gram on tcgen05 (kind::i8, int32 TMEM
- * accumulators, int64 flush): I[i*n+j] = sum_x b_i(x) b_j(x), full n x n.
- * Replaces gram_block(..., complement_cols=True) (reduction.py:75-97) as used
- * by depth_eid (depth.py:192-210): |A_i \ A_j| = I[i,i] - I[i,j]. */
+ * accumulators, int64 split reduction) from the K7 tiles (1D bulk copies):
+ * I[i*n+j] = sum_x b_i(x) b_j(x), full n x n.  Replaces
+ * gram_block(..., complement_cols=True) (reduction.py:75-97) as used by
+ * depth_eid (depth.py:192-210): |A_i \ A_j| = I[i,i] - I[i,j]. */
 size_t pidb_gram_i8_workspace_bytes(int64_t n, int64_t m);
-int pidb_gram_i8(const uint8_t* b, int64_t n, int64_t m, int64_t ldb,
-                 int64_t* gram, void* ws, size_t ws_bytes, void* stream);
-
-/* K7 + K2 in one launch (eID, unit weights): the CTAs of each K split pack
- * that split's cells to u8 (into b, (n, ldb), ldb % 128 == 0, 128-byte
- * aligned) chunk by chunk and count non-binary values (nonbinary, zero-
- * filled by the caller), while the tensor cores consume the chunks already
- * published; then the same exact int64 Gram as pidb_gram_i8.  Needs one
- * wave of CTAs: returns PIDB_EUNSUPPORTED otherwise (use pidb_binary_pack +
- * pidb_gram_i8).  Workspace: pidb_eid_gram_fused_workspace_bytes, zero-
- * filled once (its split counters return to zero). */
-size_t pidb_eid_gram_fused_workspace_bytes(int64_t n, int64_t m);
-int pidb_eid_gram_fused(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
-                        uint8_t* b, int64_t ldb, int64_t* nonbinary, int64_t* gram,
-                        void* ws, size_t ws_bytes, void* stream);
+int pidb_gram_i8(const uint8_t* tiles, int64_t n, int64_t m, int64_t* gram, void* ws,
+                 size_t ws_bytes, void* stream);
 
 /* --------------------------------------------------------------- K1x ----
  * Fixed-point Gram on the int8 tensor cores with exact integer accumulation

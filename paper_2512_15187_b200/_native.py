@@ -51,11 +51,10 @@ SIGNATURES: dict[str, tuple] = {
     "pidb_similarity_partials": (_int, [_p, _int, _i64, _i64, _i64, _p, _p, _p, _p, _p, _sz, _p]),
     "pidb_pid_colsums": (_int, [_p, _int, _i64, _i64, _i64, _p, _p, _p, _p, _sz, _p]),
     "pidb_member_masses": (_int, [_p, _int, _i64, _i64, _i64, _p, _p, _p, _p, _sz, _p]),
-    "pidb_binary_pack": (_int, [_p, _int, _i64, _i64, _i64, _p, _i64, _p, _p]),
+    "pidb_binary_pack_bytes": (_sz, [_i64, _i64]),
+    "pidb_binary_pack": (_int, [_p, _int, _i64, _i64, _i64, _p, _p, _p]),
     "pidb_gram_i8_workspace_bytes": (_sz, [_i64, _i64]),
-    "pidb_gram_i8": (_int, [_p, _i64, _i64, _i64, _p, _p, _sz, _p]),
-    "pidb_eid_gram_fused_workspace_bytes": (_sz, [_i64, _i64]),
-    "pidb_eid_gram_fused": (_int, [_p, _int, _i64, _i64, _i64, _p, _i64, _p, _p, _p, _sz, _p]),
+    "pidb_gram_i8": (_int, [_p, _i64, _i64, _p, _p, _sz, _p]),
     "pidb_gram_reduce": (_int, [_p, _i64, _p, _p, _p, _p]),
     "pidb_fixed_bytes": (_sz, [_i64, _i64]),
     "pidb_fixed_pack_workspace_bytes": (_sz, [_i64, _i64]),

@@ -12,12 +12,16 @@ namespace pidb {
 namespace {
 
 // ------------------------------------------------------------------ K7 ------
-// One warp per (member, 512-cell segment); 16-byte loads, 4-byte packed stores.
+// One warp per (member, 512-cell segment); 16-byte loads; every lane packs 16
+// cells = one 16-byte chunk of the member's 128-byte line in the 16 KB tile
+// (row block, cell block) of the tiled layout K2 reads with 1D bulk copies:
+// line i % 128 of the tile, chunk c stored at c ^ (i % 8) (128-byte swizzle).
 template <typename T>
 __global__ void binary_pack_kernel(const T* __restrict__ u, int64_t n, int64_t m, int64_t ld,
-                                   uint8_t* __restrict__ b, int64_t ldb,
+                                   uint8_t* __restrict__ tiles, int64_t nkb,
                                    unsigned long long* __restrict__ nonbinary) {
-  const int64_t segs = (ldb + 511) / 512;
+  const int64_t span = nkb * 128;  // packed cells per member (zero past m)
+  const int64_t segs = (span + 511) / 512;
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
@@ -47,8 +51,13 @@ __global__ void binary_pack_kernel(const T* __restrict__ u, int64_t n, int64_t m
       bad += !(v == T(0) || v == T(1));
       packed[e >> 2] |= (uint32_t)(v != T(0)) << (8 * (e & 3));
     }
-    if (x0 < ldb) *reinterpret_cast<uint4*>(b + i * ldb + x0) =
-        make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    if (x0 < span) {
+      const int r = (int)(i & 127);
+      const int c = (int)((x0 & 127) >> 4);
+      uint8_t* dst = tiles + ((i >> 7) * nkb + (x0 >> 7)) * (int64_t)16384 + r * 128 +
+                     (((c ^ r) & 7) << 4);
+      *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
     if (lane == 0 && bad && nonbinary) atomicAdd(&nonbinary[i], bad);
@@ -165,21 +174,28 @@ __global__ void synth_disks_kernel(float* __restrict__ out, int64_t n, int64_t r
 
 using namespace pidb;
 
+extern "C" size_t pidb_binary_pack_bytes(int64_t n, int64_t m) {
+  if (n < 1 || m < 1) return 0;
+  // row blocks of 128 members, rounded up to pairs (K2 reads 256-member B panels)
+  const int64_t nrb = 2 * ((n + 255) / 256);
+  return (size_t)nrb * (size_t)((m + 127) / 128) * 16384;
+}
+
 extern "C" int pidb_binary_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
-                                uint8_t* b, int64_t ldb, int64_t* nonbinary, void* stream) {
-  PIDB_REQUIRE(u && b && n >= 1 && m >= 1 && ld >= m, "bad arguments to pidb_binary_pack");
-  PIDB_REQUIRE(ldb >= m && ldb % 16 == 0 && (reinterpret_cast<uintptr_t>(b) & 15) == 0,
-               "packed row stride must be >= m, a multiple of 16 and 16-byte aligned");
+                                uint8_t* tiles, int64_t* nonbinary, void* stream) {
+  PIDB_REQUIRE(u && tiles && n >= 1 && m >= 1 && ld >= m, "bad arguments to pidb_binary_pack");
+  PIDB_REQUIRE((reinterpret_cast<uintptr_t>(tiles) & 1023) == 0, "tiles must be 1 KB aligned");
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t jobs = n * ((ldb + 511) / 512);
+  const int64_t nkb = (m + 127) / 128;
+  const int64_t jobs = n * ((nkb * 128 + 511) / 512);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((jobs + 7) / 8, 148 * 16));
   if (dtype == PIDB_F32)
     binary_pack_kernel<float><<<blocks, 256, 0, st>>>(
-        static_cast<const float*>(u), n, m, ld, b, ldb,
+        static_cast<const float*>(u), n, m, ld, tiles, nkb,
         reinterpret_cast<unsigned long long*>(nonbinary));
   else if (dtype == PIDB_F64)
     binary_pack_kernel<double><<<blocks, 256, 0, st>>>(
-        static_cast<const double*>(u), n, m, ld, b, ldb,
+        static_cast<const double*>(u), n, m, ld, tiles, nkb,
         reinterpret_cast<unsigned long long*>(nonbinary));
   else
     PIDB_REQUIRE(false, "dtype must be PIDB_F32 or PIDB_F64");

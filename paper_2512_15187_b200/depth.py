@@ -471,6 +471,10 @@ def _pid_factorized(de: DeviceEnsemble, out: _Out) -> torch.Tensor:
 # values have non-zero low digits; fp64 folding adds < 1e-13 relative.
 _FX_TAIL = 255.0 ** 2 * (3 * 2 ** 16 + 2 * 2 ** 8 + 1) * 2.0 ** -62
 _FX_REL = 1e-13
+# Certified accuracy of depth_pid(algorithm="gram"): members whose bound
+# exceeds it (members with tiny mass next to heavy ones, e.g. one-cell grids)
+# are resolved with the exact path like uncertified ranks.
+GRAM_DEPTH_TOL = 1e-8
 
 # Diagnostics of the last tensor-core PID on this process (read by bench.py):
 # certified bound, members resolved exactly.
@@ -524,8 +528,9 @@ def _pid_gram(de: DeviceEnsemble, out: _Out) -> np.ndarray:
     and inverse-mass-weighted column sums of G (depth.py:156-160) fused into
     the Gram epilogue: no N x N matrix in HBM.  Then the rank certifier
     (SURVEY.md §7.3): every member whose depth interval (rigorous Gram error
-    bound) meets another member's is resolved with the exact fp64 path, so
-    the ranks equal the exact ones.  Returns the masses."""
+    bound) meets another member's, or whose bound exceeds GRAM_DEPTH_TOL, is
+    resolved with the exact fp64 path, so the ranks equal the exact ones and
+    every depth is within GRAM_DEPTH_TOL of exact.  Returns the masses."""
     from .reduction import pack_fixed
 
     n, dev = de.n, de.device
@@ -563,7 +568,7 @@ def _pid_gram(de: DeviceEnsemble, out: _Out) -> np.ndarray:
         m_cells = float(de.m)
     eps = _gram_depth_bounds(masses, soft.cpu().numpy(), h[:n], rch[:n], rch[n:], m_cells,
                              wmax, wmin)
-    flag = _clustered(h[3 * n:4 * n], eps)
+    flag = _clustered(h[3 * n:4 * n], eps) | (eps > GRAM_DEPTH_TOL)
     LAST_GRAM_CERT.clear()
     LAST_GRAM_CERT.update(max_bound=float(eps.max()), resolved_exactly=int(flag.sum()))
     if flag.any():
@@ -614,44 +619,6 @@ def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") 
     return _finish(de, out, "pid", masses, t0)
 
 
-# K7 fused into the K2 launch: correct (tests/test_gpu_parity.py) but measured
-# slower at cfg2 than the two kernels (0.178 vs 0.168 ms: 16 packer warps per
-# SM stream the members at ~3 TB/s, the standalone pack at ~6.8 TB/s;
-# profiles/r02_eid_fused_ab.log), so it is opt-in: PIDB_EID_FUSED=1.
-_FUSED_EID = os.environ.get("PIDB_EID_FUSED", "0") == "1"
-
-
-def _eid_gram_fused(de: DeviceEnsemble, nb: torch.Tensor):
-    """K7 + K2 in one launch (pidb_eid_gram_fused); None when the shape needs
-    more than one wave of CTAs (then pack and Gram run as two kernels)."""
-    if not _FUSED_EID:
-        return None
-    lib = N.load()
-    ldb = (de.m + 127) // 128 * 128
-    key = ("eid_u8", ldb)
-    b = de._cache.get(key)
-    if b is None or torch.cuda.is_current_stream_capturing():
-        b = torch.empty((de.n, ldb), dtype=torch.uint8, device=de.device)
-        if not torch.cuda.is_current_stream_capturing():
-            de._cache[key] = b
-    g = torch.empty((de.n, de.n), dtype=torch.int64, device=de.device)
-    ws = de.workspace(lib.pidb_eid_gram_fused_workspace_bytes(de.n, de.m))
-    ev = None
-    if KERNEL_EVENTS is not None:
-        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-        ev[0].record()
-    rc = lib.pidb_eid_gram_fused(de.ptr(), de.dtype_code, de.n, de.m, de.ld, b.data_ptr(), ldb,
-                                 nb.data_ptr(), g.data_ptr(), ws.data_ptr(), ws.numel(),
-                                 stream_ptr(de.device))
-    if rc == N.PIDB_EUNSUPPORTED:
-        return None
-    N.check(rc, "pidb_eid_gram_fused")
-    if ev is not None:
-        ev[1].record()
-        KERNEL_EVENTS.append(("pidb_eid_gram_fused", *ev))
-    return g
-
-
 def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
     """Inclusion depth of binary ensembles (depth.py:192-210).
 
@@ -669,19 +636,13 @@ def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
         def enqueue():
             # K7 packs and counts non-binary values in the same pass (the
             # counts ride in the result block); the masses are the Gram
-            # diagonal |C_i| (exact integers).  One wave fits: K7 fused into
-            # the K2 launch (pack and Gram overlap), else the two kernels.
+            # diagonal |C_i| (exact integers)
             out = _Out(n, dev, extra=n)
             nb = out.extra.view(torch.int64)
             nb.zero_()
-            g = _eid_gram_fused(de, nb)
-            if g is None:
-                packed = pack_binary(de, nb)
-                _allreduce(nb, de)
-                g = intersection_gram(de, packed)
-            else:
-                _allreduce(nb, de)
-                _allreduce(g, de)
+            packed = pack_binary(de, nb)
+            _allreduce(nb, de)
+            g = intersection_gram(de, packed)
             mslot, ii, io, d = out.ptrs()
             N.call("pidb_eid_exact_epilogue", g.data_ptr(), n, ii, io, d, out.rank.data_ptr(),
                    mslot, stream_ptr(dev))

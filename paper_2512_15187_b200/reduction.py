@@ -43,13 +43,7 @@ def pack_fixed(de: DeviceEnsemble, soft: torch.Tensor | None = None,
     the same pass.  The digit buffer (zero-filled once: rows
     past n stay zero) is kept on the ensemble and re-packed on every call
     (the members may change in place)."""
-    nbytes = int(N.load().pidb_fixed_bytes(de.n, de.m))
-    q = de._cache.get("fixed_q")
-    if q is None or q.numel() != nbytes:
-        buf = torch.zeros(nbytes + 1024, dtype=torch.uint8, device=de.device)
-        off = (-buf.data_ptr()) % 1024  # 1 KB aligned tiles (swizzle atoms)
-        q = buf[off:off + nbytes]
-        de._cache["fixed_q"] = q
+    q = de.scratch("k1x_digits", int(N.load().pidb_fixed_bytes(de.n, de.m)))
     wmax = de._cache.get("fixed_wmax")
     if wmax is None:
         wmax = float(de.weights.max()) if de.weights is not None else 1.0
@@ -84,14 +78,14 @@ def gram_device(de: DeviceEnsemble) -> torch.Tensor:
 
 
 def pack_binary(de: DeviceEnsemble, nonbinary: torch.Tensor | None = None) -> torch.Tensor:
-    """K7: 0/1 members -> uint8 rows (row stride a multiple of 128 bytes);
-    optionally counts each member's values that are neither 0 nor 1
-    (`nonbinary`, int64 (n,) zero-filled by the caller)."""
-    ldb = (de.m + 127) // 128 * 128
-    b = torch.empty((de.n, ldb), dtype=torch.uint8, device=de.device)
+    """K7: 0/1 members -> u8 tiles for K2 (include/pidb.h); optionally counts
+    each member's values that are neither 0 nor 1 (`nonbinary`, int64 (n,)
+    zero-filled by the caller).  The tile buffer is zero-filled once (padding
+    rows stay zero) and kept on the ensemble; it is re-packed on every call."""
+    b = de.scratch("k7_tiles", int(N.load().pidb_binary_pack_bytes(de.n, de.m)))
     from .depth import _launch
 
-    _launch("pidb_binary_pack", de.ptr(), de.dtype_code, de.n, de.m, de.ld, b.data_ptr(), ldb,
+    _launch("pidb_binary_pack", de.ptr(), de.dtype_code, de.n, de.m, de.ld, b.data_ptr(),
             None if nonbinary is None else nonbinary.data_ptr(), stream_ptr(de.device))
     return b
 
@@ -104,18 +98,10 @@ def intersection_gram(de: DeviceEnsemble, packed: torch.Tensor | None = None) ->
     ws = de.workspace(lib.pidb_gram_i8_workspace_bytes(de.n, de.m))
     from .depth import _launch
 
-    _launch("pidb_gram_i8", b.data_ptr(), de.n, de.m, b.stride(0), g.data_ptr(),
-           ws.data_ptr(), ws.numel(), stream_ptr(de.device))
+    _launch("pidb_gram_i8", b.data_ptr(), de.n, de.m, g.data_ptr(), ws.data_ptr(), ws.numel(),
+            stream_ptr(de.device))
     _allreduce(g, de)
     return g
-
-
-_EXACT_F32 = (np.float32, np.float16, np.bool_, np.uint8, np.int8, np.uint16, np.int16)
-
-
-def _block_to_device(a, dt, dev) -> torch.Tensor:
-    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
-    return t.to(device=dev, dtype=dt).contiguous()
 
 
 def gram_block(rows, cols, weights=None, complement_cols: bool = False) -> np.ndarray:
