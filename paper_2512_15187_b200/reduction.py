@@ -104,6 +104,14 @@ def intersection_gram(de: DeviceEnsemble, packed: torch.Tensor | None = None) ->
     return g
 
 
+_EXACT_F32 = (np.float32, np.float16, np.bool_, np.uint8, np.int8, np.uint16, np.int16)
+
+
+def _block_to_device(a, dt, dev) -> torch.Tensor:
+    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+    return t.to(device=dev, dtype=dt).contiguous()
+
+
 def gram_block(rows, cols, weights=None, complement_cols: bool = False) -> np.ndarray:
     """Array-level drop-in for gram_block (reduction.py:75-97), in fp64.
 
