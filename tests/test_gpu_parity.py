@@ -872,4 +872,10 @@ def test_pid_gram_certified_tolerance_tiny_masses(pb, n, m, seed):
     a = pb.depth_pid(e, algorithm="gram")
     want = port.depth_pid(U)
     close(a.depth, want["depth"], D.GRAM_DEPTH_TOL)
-    np.testing.assert_array_equal(a.rank, want["rank"])
+    # one-cell grids tie every member whose value exceeds the mean (depth =
+    # mean exactly), and the oracle breaks those ties by rounding noise: the
+    # ranking must order every pair whose exact depths differ by > 1e-12
+    order = np.argsort(a.rank)
+    assert np.all(np.diff(want["depth"][order]) <= 1e-12)
+    if m > 1:
+        np.testing.assert_array_equal(a.rank, want["rank"])
