@@ -358,7 +358,7 @@ STREAM_SLAB_BYTES = int(os.environ.get("PIDB_STREAM_SLAB_BYTES", str(2 << 30)))
 
 def _streamable(x) -> bool:
     return (isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.dim() >= 2
-            and x.dtype in (torch.float32, torch.float64) and x.shape[0] >= 1
+            and x.is_contiguous() and x.dtype in (torch.float32, torch.float64) and x.shape[0] >= 1
             and x.numel() * x.element_size() > 2 * STREAM_SLAB_BYTES)
 
 

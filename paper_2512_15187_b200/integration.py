@@ -43,6 +43,8 @@ def install(fd=None) -> list[str]:
     B200 implementation; returns the rebound ``module.name`` list."""
     if fd is None:
         import fuzzdepth as fd  # noqa: F811
+    if _saved:  # already installed: keep the true originals for uninstall()
+        return sorted(f"{m}.{n}" for m, n in _saved)
     base = fd.__name__
     originals = {}
     for sub, names in _ROUTES.items():

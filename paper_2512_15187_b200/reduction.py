@@ -136,9 +136,11 @@ def gram_block(rows, cols, weights=None, complement_cols: bool = False) -> np.nd
         return np.zeros((nr, nc), dtype=np.float64)
     dev = require_cuda()
 
-    def exact32(a):
-        d = a.dtype if isinstance(a, np.ndarray) else torch.empty(0, dtype=a.dtype).numpy().dtype
-        return any(d == np.dtype(t) for t in _EXACT_F32)
+    def exact32(a):  # values exactly representable in float32
+        if isinstance(a, torch.Tensor):
+            return a.dtype in (torch.float32, torch.float16, torch.bfloat16, torch.bool,
+                               torch.uint8, torch.int8, torch.int16)
+        return any(a.dtype == np.dtype(t) for t in _EXACT_F32)
 
     f32 = exact32(rows) and exact32(cols)
     dt = torch.float32 if f32 else torch.float64

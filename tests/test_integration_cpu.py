@@ -34,6 +34,7 @@ def test_install_rebinds_every_depth_path_binding(fd):
 
     orig = fd.depth.depth_pid
     done = integration.install(fd)
+    assert integration.install(fd) == done  # idempotent: originals kept
     try:
         for want in ("fuzzdepth.depth.depth_pid", "fuzzdepth.depth_pid_mean",
                      "fuzzdepth.depth.depth_eid", "fuzzdepth.consistency.depth_by_method",
