@@ -365,6 +365,8 @@ def run_reference(args, rank, world):
 
 # central planes of 512^3 in the CPU samples (reference arm, cpu_baseline)
 REF_PLANES = 16
+# end-to-end steps (each moves the whole ensemble over PCIe: ~2 s at cfg5)
+E2E_STEPS = 10
 
 
 def ncu_traffic(workload, world):
@@ -601,7 +603,7 @@ def run_e2e(args, host, _, meta, fn, world, pg, dev):
                                        cell_range=cr if world > 1 else None, device=dev)
         return fn(e)
 
-    ms = timed(step, max(10, args.steps), 3, world)
+    ms = timed(step, E2E_STEPS, 3, world)
     total = n * int(np.prod(dims))
     path = ("depth_pid_mean(pinned host tensor): cell slabs of "
             f"{D.STREAM_SLAB_BYTES >> 20} MB, H2D on a side stream overlapped with in-place "
@@ -610,7 +612,7 @@ def run_e2e(args, host, _, meta, fn, world, pg, dev):
             "DeviceEnsemble.from_tensor(pinned host tensor) (pitched H2D + device validation) "
             "+ the method + result D2H")
     return {"value": total / (ms * 1e-3), "unit": "member-voxels/s", "ms_per_step": ms,
-            "steps": max(10, args.steps), "warmup": 3,
+            "steps": E2E_STEPS, "warmup": 3,
             "h2d_bytes_per_step": n * m * 4, "d2h_bytes_per_step": (5 * n + n + 1) * 8,
             "h2d_GBps_effective": n * m * 4 / (ms * 1e-3) / 1e9,
             "bound": "PCIe host-to-device copy", "path": path}
