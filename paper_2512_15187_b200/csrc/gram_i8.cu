@@ -141,25 +141,32 @@ __global__ void __launch_bounds__(kGramThreads, 1)
 }
 
 // I[i][j] = I[j][i] = sum over splits of the tile holding (i, j), i <= j.
-// Each upper-triangle entry is summed once (reads coalesced along j) and
-// written to both halves; int64 sums are exact, so the order is immaterial.
-__global__ void gram_i8_reduce_kernel(const int32_t* __restrict__ part, int n, int nib,
-                                      int splits, int64_t* __restrict__ out) {
-  const int64_t total = (int64_t)n * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
-    if (i > j) continue;
-    const int ib = i / kBM, jb = j / kBN;
-    int t = 0;
-    for (int q = 0; q < jb; ++q) t += min(nib, 2 * q + 2);
-    t += ib;
-    const int32_t* src = part + ((size_t)t * splits * kBM + (i - ib * kBM)) * kBN + (j - jb * kBN);
-    int64_t acc = 0;
-#pragma unroll 8
-    for (int s = 0; s < splits; ++s) acc += __ldg(src + (size_t)s * kBM * kBN);
-    out[e] = acc;
-    if (i != j) out[(int64_t)j * n + i] = acc;
+// One thread per (tile, tile row, 4 consecutive columns): 16-byte partial
+// loads along the row (coalesced), int64 sums (exact, any order), the upper
+// entries written along the row and mirrored into the lower triangle.
+__global__ void __launch_bounds__(256)
+    gram_i8_reduce_kernel(const int32_t* __restrict__ part, int n, int nib, int splits,
+                          int64_t* __restrict__ out) {
+  const int t = blockIdx.x >> 5;                      // tile
+  const int r = ((blockIdx.x & 31) << 2) + (threadIdx.x >> 6);  // tile row 0..127
+  const int c4 = (threadIdx.x & 63) << 2;             // first of 4 tile columns
+  int ib, jb;
+  tile_of(t, nib, ib, jb);
+  const int i = ib * kBM + r, j0 = jb * kBN + c4;
+  if (i >= n || j0 >= n || j0 + 3 < i) return;
+  const int4* src = reinterpret_cast<const int4*>(part + ((size_t)t * splits * kBM + r) * kBN + c4);
+  long long acc[4] = {0, 0, 0, 0};
+#pragma unroll 4
+  for (int s = 0; s < splits; ++s) {
+    const int4 v = __ldg(src + (size_t)s * kBM * kBN / 4);
+    acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = j0 + k;
+    if (j >= n || j < i) continue;
+    out[(int64_t)i * n + j] = acc[k];
+    if (j != i) out[(int64_t)j * n + i] = acc[k];
   }
 }
 
@@ -214,9 +221,7 @@ extern "C" int pidb_gram_i8(const uint8_t* tiles, int64_t n, int64_t m, int64_t*
                                  (int)g.smem));
   gram_i8_kernel<<<g.units, kGramThreads, g.smem, st>>>(tiles, p);
   PIDB_LAUNCH_CHECK("gram_i8_kernel");
-  const int64_t total = n * n;
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
-  gram_i8_reduce_kernel<<<blocks, 256, 0, st>>>(p.part, (int)n, g.nib, g.splits, gram);
+  gram_i8_reduce_kernel<<<g.ntiles * 32, 256, 0, st>>>(p.part, (int)n, g.nib, g.splits, gram);
   PIDB_LAUNCH_CHECK("gram_i8_reduce_kernel");
   return PIDB_OK;
 }
