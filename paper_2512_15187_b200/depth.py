@@ -77,11 +77,16 @@ def ranks_from_depths(depth: np.ndarray) -> np.ndarray:
 
 
 def mass_cv(masses: np.ndarray) -> float:
-    """Population std / mean of member masses (depth.py:105-110)."""
-    mean = float(np.mean(masses))
+    """Population std / mean of member masses (depth.py:105-110).  The same
+    two-pass arithmetic as np.std (pairwise mean, then the mean square
+    deviation) without its per-call overhead (~20 us on small ensembles)."""
+    m = np.asarray(masses, dtype=np.float64)
+    n = m.shape[0]
+    mean = float(m.sum()) / n
     if mean == 0.0:
         return 0.0
-    return float(np.std(masses) / mean)
+    d = m - mean
+    return float(np.sqrt(float(np.dot(d, d)) / n) / mean)
 
 
 def resolve_workers(workers: int | None = None) -> int:
@@ -96,7 +101,10 @@ def resolve_workers(workers: int | None = None) -> int:
             return max(1, int(env))
         except ValueError:
             pass
-    return os.cpu_count() or 1
+    return _CPU_COUNT
+
+
+_CPU_COUNT = os.cpu_count() or 1
 
 
 # --------------------------------------------------------------- primitives
@@ -159,6 +167,7 @@ def _graphed(de: DeviceEnsemble, key: str, enqueue) -> "_Out":
             for ws in de._cache.pop("graph_ws_pending", []):
                 ws.zero_()  # the kernels leave their counters at zero after each replay
                 de._cache.setdefault("graph_ws", []).append(ws)
+            outs._pinned = torch.empty(outs.block.shape, dtype=outs.block.dtype, pin_memory=True)
             ent = cache[skey] = (g, outs, threading.Lock())
     if ent is None:
         out = enqueue()
@@ -243,6 +252,7 @@ class _Out:
         self.rank = self.block[4 * n:5 * n].view(torch.int64)
         self.extra = self.block[5 * n:]
         self._host = None
+        self._pinned = None  # pinned staging for the D2H (graph-replayed blocks)
 
     def ptrs(self):
         p, n = self.vals.data_ptr(), self.n
@@ -251,7 +261,13 @@ class _Out:
     def host(self) -> np.ndarray:
         h = self._host
         if h is None:
-            h = self._host = self.block.cpu().numpy()
+            pin = self._pinned
+            if pin is None:
+                h = self._host = self.block.cpu().numpy()
+            else:  # async D2H into pinned memory, then a private host copy
+                pin.copy_(self.block, non_blocking=True)
+                torch.cuda.current_stream(self.block.device).synchronize()
+                h = self._host = pin.numpy().copy()
         return h
 
     def fresh(self) -> "_Out":
