@@ -34,8 +34,9 @@
 // (tools/fixed_gram_emulation.py): depth error <= 3.2e-9 at N = 300 with
 // uniform, u^8 and ellipsoid members, 0 rank swaps.
 //
-// Work: 128 x 128 tiles of the upper block triangle x split-K (one wave);
-// diagonal tiles load one operand.  Warps (576 threads): 0 TMA producer
+// Work: 128 x 128 tiles of the upper block triangle x K rounds, persistent
+// CTAs over the (round, tile) units (all 148 SMs busy with equal work where
+// the counts allow); diagonal tiles load one operand.  Warps (576 threads): 0 TMA producer
 // (6-stage ring, 32 KB per stage), 1 MMA issuer, 2-17 epilogue (TMEM lane
 // quadrant = warp % 4, 32 columns each).  Outputs per (tile, split) unit:
 // the fp64 tile, or (PID) its row sums, inverse-mass-weighted row sums and
@@ -61,14 +62,33 @@ constexpr int kThreads = (2 + kEpiWarps) * 32;
 constexpr uint32_t kIdesc = tc::idesc(tc::kCS32, tc::kU8, kB, kB);
 constexpr double kTwoPow31 = 2147483648.0;
 
+// Work units: (K round q, tile t), q-major (unit u = q ntiles + t); the K
+// range is cut into `rounds` windows of R blocks (the last Rl).  Persistent
+// CTAs take units u = c, c + G, c + 2G, ...: with rounds chosen so that the
+// unit count is a multiple of the grid (lcm(ntiles, SMs) / ntiles when the
+// windows stay >= 256 blocks) every SM gets the same work, and the CTAs
+// running together still read the same few K windows of the operand panels
+// (L2 reuse across tiles; a stream-K line with staggered K offsets lost it:
+// 52 -> 85 ms at cfg4).  One output slot per unit, reduced per tile in round
+// order.
 struct FxParams {
-  int n, nib, ntiles, splits, kblocks, kb_per;
-  int flush;          // stages per int32 window (kFlush; A/B hook PIDB_FX_FLUSH)
-  int noload;         // A/B hook PIDB_FX_NOLOAD=1: skip the TMA loads (timing only)
-  int sums;           // 1: tile sums (PID), 0: fp64 tiles
-  const double* inv;  // sums: inverse masses (n)
-  double* part;       // sums: [units][4][kB]; tiles: [units][kB][kB]
+  int n, nib, ntiles, kblocks;
+  int rounds, R, Rl;   // K windows: rounds - 1 of R blocks, then Rl
+  int64_t units;       // rounds * ntiles
+  int flush;           // stages per int32 window (kFlush; A/B hook PIDB_FX_FLUSH)
+  int noload;          // A/B hook PIDB_FX_NOLOAD=1: skip the operand loads (timing only)
+  int sums;            // 1: tile sums (PID), 0: fp64 tiles
+  const double* inv;   // sums: inverse masses (n)
+  double* part;        // sums: [units][4][kB]; tiles: [units][kB][kB]
 };
+
+__host__ __device__ __forceinline__ void fx_unit(const FxParams& p, int64_t u, int& t, int& kb0,
+                                                 int& nk) {
+  const int q = (int)(u / p.ntiles);
+  t = (int)(u - (int64_t)q * p.ntiles);
+  kb0 = q * p.R;
+  nk = q < p.rounds - 1 ? p.R : p.Rl;
+}
 
 __host__ __device__ __forceinline__ void fx_tile(int t, int& ib, int& jb) {
   int j = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
@@ -257,18 +277,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int unit = blockIdx.x;
-  const int t = unit % p.ntiles, split = unit / p.ntiles;  // split-major: one K window at a time
-  int ib, jb;
-  fx_tile(t, ib, jb);
-  const bool diag = ib == jb;
-  const int kb0 = split * p.kb_per;
-  const int nk = max(0, min(p.kblocks, kb0 + p.kb_per) - kb0);
   const int fl = p.flush;
-  const int nflush = (nk + fl - 1) / fl;
+  uint64_t* ring_free = tempty + 1;  // epilogue done with the ring (after a segment)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -277,6 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, kEpiWarps);
+    mbar_init(ring_free, 1);
     fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -288,117 +302,147 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (tc::elect_one()) {
       const uint64_t pol = policy_evict_last();  // panels are re-read by the other tiles
-      const uint32_t bytes = diag ? kTileBytes : kStageBytes;
-      int s = 0;
+      int s = 0, seg = 0;
       uint32_t ph = 0;
-      for (int k = 0; k < nk; ++k) {
-        mbar_wait(&empty[s], ph ^ 1u);
-        unsigned char* a = ring + s * kStageBytes;
-        if (p.noload) {
-          mbar_arrive(&full[s]);
-        } else {
-          mbar_arrive_expect_tx(&full[s], bytes);
-          const int64_t kb = kb0 + k;
-          bulk_load(a, qd + ((int64_t)ib * p.kblocks + kb) * kTileBytes, kTileBytes, &full[s], pol);
-          if (!diag)
-            bulk_load(a + kTileBytes, qd + ((int64_t)jb * p.kblocks + kb) * kTileBytes, kTileBytes,
-                      &full[s], pol);
+      for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++seg) {
+        int t, kb0, nk, ib, jb;
+        fx_unit(p, u, t, kb0, nk);
+        fx_tile(t, ib, jb);
+        const bool diag = ib == jb;
+        const uint32_t bytes = diag ? kTileBytes : kStageBytes;
+        // the previous segment's epilogue stages its fp64 tile in the ring
+        if (seg > 0) mbar_wait(ring_free, (uint32_t)((seg - 1) & 1));
+        for (int k = 0; k < nk; ++k) {
+          mbar_wait(&empty[s], ph ^ 1u);
+          unsigned char* a = ring + s * kStageBytes;
+          if (p.noload) {
+            mbar_arrive(&full[s]);
+          } else {
+            mbar_arrive_expect_tx(&full[s], bytes);
+            const int64_t kb = kb0 + k;
+            bulk_load(a, qd + ((int64_t)ib * p.kblocks + kb) * kTileBytes, kTileBytes, &full[s],
+                      pol);
+            if (!diag)
+              bulk_load(a + kTileBytes, qd + ((int64_t)jb * p.kblocks + kb) * kTileBytes,
+                        kTileBytes, &full[s], pol);
+          }
+          if (++s == kStages) { s = 0; ph ^= 1u; }
         }
-        if (++s == kStages) { s = 0; ph ^= 1u; }
       }
     }
   } else if (warp == 1) {
     if (tc::elect_one()) {
-      int s = 0;
+      int s = 0, win = 0;
       uint32_t ph = 0;
-      for (int k = 0; k < nk; ++k) {
-        const int kw = k % fl;
-        if (kw == 0 && k > 0) {
-          mbar_wait(tempty, (uint32_t)((k / fl - 1) & 1));  // epilogue drained TMEM
+      for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+        int t, kb0, nk, ib, jb;
+        fx_unit(p, u, t, kb0, nk);
+        fx_tile(t, ib, jb);
+        const bool diag = ib == jb;
+        for (int k = 0; k < nk; ++k) {
+          const int kw = k % fl;
+          if (kw == 0 && win > 0) {
+            mbar_wait(tempty, (uint32_t)((win - 1) & 1));  // epilogue drained TMEM
+            tc::fence_after();
+          }
+          mbar_wait(&full[s], ph);
           tc::fence_after();
+          const uint32_t a = smem_u32(ring + s * kStageBytes);
+          const uint64_t da = tc::desc_kmajor_sw128(a);
+          const uint64_t db = diag ? da : tc::desc_kmajor_sw128(a + kTileBytes);
+          const uint32_t acc = kw != 0;
+          // level s = k + l accumulates at TMEM column 128 s; digit plane k is
+          // the descriptor advanced by 32 bytes (2 x 16-byte units) per plane
+#pragma unroll
+          for (int lv = 0; lv < 4; ++lv)
+#pragma unroll
+            for (int dk = 0; dk <= lv; ++dk)
+              tc::mma_i8(tmem + 128u * lv, da + 2 * dk, db + 2 * (lv - dk), kIdesc,
+                         dk != 0 ? 1u : acc);
+          tc::commit(&empty[s]);
+          if (kw == fl - 1 || k == nk - 1) {
+            tc::commit(tfull);
+            ++win;
+          }
+          if (++s == kStages) { s = 0; ph ^= 1u; }
         }
-        mbar_wait(&full[s], ph);
-        tc::fence_after();
-        const uint32_t a = smem_u32(ring + s * kStageBytes);
-        const uint64_t da = tc::desc_kmajor_sw128(a);
-        const uint64_t db = diag ? da : tc::desc_kmajor_sw128(a + kTileBytes);
-        const uint32_t acc = kw != 0;
-        // level s = k + l accumulates at TMEM column 128 s; digit plane k is
-        // the descriptor advanced by 32 bytes (2 x 16-byte units) per plane
-#pragma unroll
-        for (int lv = 0; lv < 4; ++lv)
-#pragma unroll
-          for (int dk = 0; dk <= lv; ++dk)
-            tc::mma_i8(tmem + 128u * lv, da + 2 * dk, db + 2 * (lv - dk), kIdesc,
-                       dk != 0 ? 1u : acc);
-        tc::commit(&empty[s]);
-        if (kw == fl - 1 || k == nk - 1) tc::commit(tfull);
-        if (++s == kStages) { s = 0; ph ^= 1u; }
       }
     }
   } else {
     // epilogue: TMEM lane quadrant q (hardware rule: warp % 4), columns c0..c0+31
     const int q = warp & 3, cc = (warp - 2) >> 2;
     const int row = q * 32 + lane, c0 = cc * 32;
+    const int et = threadIdx.x - 64;  // 0..511
     const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
-    double acc[32];
+    int win = 0;
+    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+      int t, kb0, nk, ib, jb;
+      fx_unit(p, u, t, kb0, nk);
+      fx_tile(t, ib, jb);
+      const bool diag = ib == jb;
+      const int nflush = (nk + fl - 1) / fl;
+      double acc[32];
 #pragma unroll
-    for (int e = 0; e < 32; ++e) acc[e] = 0.0;
-    for (int f = 0; f < nflush; ++f) {
-      mbar_wait(tfull, (uint32_t)(f & 1));
-      tc::fence_after();
+      for (int e = 0; e < 32; ++e) acc[e] = 0.0;
+      for (int f = 0; f < nflush; ++f, ++win) {
+        mbar_wait(tfull, (uint32_t)(win & 1));
+        tc::fence_after();
 #pragma unroll
-      for (int h = 0; h < 8; ++h) {
-        // v = ((L0 * 256 + L1) * 256 + L2) * 256 + L3: integers < 2^53, exact in fp64
-        double v[4];
+        for (int h = 0; h < 8; ++h) {
+          // v = ((L0 * 256 + L1) * 256 + L2) * 256 + L3: integers < 2^53, exact in fp64
+          uint32_t r[4][4];
 #pragma unroll
-        for (int lv = 0; lv < 4; ++lv) {
-          uint32_t r[4];
-          tc::tmem_ld4(tbase + 128u * lv + 4u * h, r);
+          for (int lv = 0; lv < 4; ++lv) tc::tmem_ld4(tbase + 128u * lv + 4u * h, r[lv]);
           tc::tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            v[e] = lv == 0 ? (double)(int32_t)r[e] : fma(v[e], 256.0, (double)(int32_t)r[e]);
-        }
+          for (int e = 0; e < 4; ++e) {
+            double v = (double)(int32_t)r[0][e];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[4 * h + e] += v[e];
+            for (int lv = 1; lv < 4; ++lv) v = fma(v, 256.0, (double)(int32_t)r[lv][e]);
+            acc[4 * h + e] += v;
+          }
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
       }
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);
-    }
 
-    // All stages are consumed: stage the fp64 tile in the free ring (row
-    // stride kB + 1 doubles), then sum / store it in a fixed order.
-    double* tile = reinterpret_cast<double*>(ring);
-    constexpr int kLd = kB + 1;
+      // All of the segment's stages are consumed: stage the fp64 tile in the
+      // ring (row stride kB + 1 doubles), then sum / store it in a fixed order.
+      double* tile = reinterpret_cast<double*>(ring);
+      constexpr int kLd = kB + 1;
 #pragma unroll
-    for (int e = 0; e < 32; ++e) tile[row * kLd + c0 + e] = acc[e];
-    epi_sync();
-    const int et = threadIdx.x - 64;  // 0..511
-    if (!p.sums) {
-      double* dst = p.part + (size_t)unit * kB * kB;
-      for (int e = et; e < kB * kB; e += kEpiWarps * 32) dst[e] = tile[(e / kB) * kLd + (e % kB)];
-    } else {
-      // et / 128 = 0: row sums, 1: rows weighted by inv_j, 2: column sums,
-      // 3: columns weighted by inv_i (off-diagonal tiles only)
-      const int kind = et >> 7, r = et & (kB - 1);
-      double s2 = 0.0;
-      if (kind == 0) {
-        for (int c = 0; c < kB; ++c) s2 += tile[r * kLd + c];
-      } else if (kind == 1) {
-        for (int c = 0; c < kB; ++c) {
-          const int gj = jb * kB + c;
-          s2 += (gj < p.n ? __ldg(p.inv + gj) : 0.0) * tile[r * kLd + c];
+      for (int e = 0; e < 32; ++e) tile[row * kLd + c0 + e] = acc[e];
+      epi_sync();
+      const int64_t slot = u;
+      if (!p.sums) {
+        double* dst = p.part + (size_t)slot * kB * kB;
+        for (int e = et; e < kB * kB; e += kEpiWarps * 32) dst[e] = tile[(e / kB) * kLd + (e % kB)];
+      } else {
+        // et / 128 = 0: row sums, 1: rows weighted by inv_j, 2: column sums,
+        // 3: columns weighted by inv_i (off-diagonal tiles only)
+        const int kind = et >> 7, r = et & (kB - 1);
+        double s2 = 0.0;
+        if (kind == 0) {
+          for (int c = 0; c < kB; ++c) s2 += tile[r * kLd + c];
+        } else if (kind == 1) {
+          for (int c = 0; c < kB; ++c) {
+            const int gj = jb * kB + c;
+            s2 += (gj < p.n ? __ldg(p.inv + gj) : 0.0) * tile[r * kLd + c];
+          }
+        } else if (!diag) {
+          for (int x = 0; x < kB; ++x) {
+            const int gi = ib * kB + x;
+            const double wgt = kind == 2 ? 1.0 : (gi < p.n ? __ldg(p.inv + gi) : 0.0);
+            s2 += wgt * tile[x * kLd + r];
+          }
         }
-      } else if (!diag) {
-        for (int x = 0; x < kB; ++x) {
-          const int gi = ib * kB + x;
-          const double wgt = kind == 2 ? 1.0 : (gi < p.n ? __ldg(p.inv + gi) : 0.0);
-          s2 += wgt * tile[x * kLd + r];
-        }
+        p.part[(size_t)slot * 4 * kB + et] = s2;
       }
-      p.part[(size_t)unit * 4 * kB + et] = s2;
+      // hand the ring back to the producer (generic -> async proxy)
+      fence_proxy_async_smem();
+      epi_sync();
+      if (et == 0) mbar_arrive(ring_free);
     }
   }
   tc::fence_before();
@@ -406,49 +450,51 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
+// Every slot of tile t (one unit per K round), in round order (fixed).
+template <typename F>
+__device__ __forceinline__ void fx_for_slots(const FxParams& p, int t, F&& f) {
+  for (int q = 0; q < p.rounds; ++q) f((int64_t)q * p.ntiles + t);
+}
+
 // PID sums: row_plain[i] = sum_j G[i,j], col_inv[i] = sum_j inv_j G[i,j]
 // (G symmetric), over the tiles holding member i as a row (ib, jb >= ib) or
-// as a column (a < ib, ib), splits inner, in that fixed order.
-__global__ void fx_sums_reduce_kernel(const double* __restrict__ part, int n, int nib, int ntiles,
-                                      int splits, double scale, double* __restrict__ row_plain,
+// as a column (a < ib, ib).
+__global__ void fx_sums_reduce_kernel(const FxParams p, double scale,
+                                      double* __restrict__ row_plain,
                                       double* __restrict__ col_inv) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= p.n) return;
   const int ib = i / kB, r = i - ib * kB;
   double a = 0.0, b = 0.0;
-  for (int jb = ib; jb < nib; ++jb) {
-    const int t = jb * (jb + 1) / 2 + ib;
-    for (int s = 0; s < splits; ++s) {
-      const double* u = part + ((size_t)s * ntiles + t) * 4 * kB;
+  for (int jb = ib; jb < p.nib; ++jb)
+    fx_for_slots(p, jb * (jb + 1) / 2 + ib, [&](int64_t slot) {
+      const double* u = p.part + (size_t)slot * 4 * kB;
       a += u[r];
       b += u[kB + r];
-    }
-  }
-  for (int x = 0; x < ib; ++x) {
-    const int t = ib * (ib + 1) / 2 + x;
-    for (int s = 0; s < splits; ++s) {
-      const double* u = part + ((size_t)s * ntiles + t) * 4 * kB;
+    });
+  for (int x = 0; x < ib; ++x)
+    fx_for_slots(p, ib * (ib + 1) / 2 + x, [&](int64_t slot) {
+      const double* u = p.part + (size_t)slot * 4 * kB;
       a += u[2 * kB + r];
       b += u[3 * kB + r];
-    }
-  }
+    });
   row_plain[i] = a * scale;
   col_inv[i] = b * scale;
 }
 
-// G[i][j] = G[j][i] = scale * sum over splits of the tile holding (i, j), i <= j.
-__global__ void fx_tiles_reduce_kernel(const double* __restrict__ part, int n, int ntiles,
-                                       int splits, double scale, double* __restrict__ out) {
+// G[i][j] = G[j][i] = scale * sum over the slots of the tile holding (i, j), i <= j.
+__global__ void fx_tiles_reduce_kernel(const FxParams p, double scale, double* __restrict__ out) {
+  const int n = p.n;
   const int64_t total = (int64_t)n * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
     if (i > j) continue;
     const int ib = i / kB, jb = j / kB;
-    const int t = jb * (jb + 1) / 2 + ib;
-    const double* src = part + ((size_t)t * kB + (i - ib * kB)) * kB + (j - jb * kB);
     double acc = 0.0;
-    for (int s = 0; s < splits; ++s) acc += src[(size_t)s * ntiles * kB * kB];
+    fx_for_slots(p, jb * (jb + 1) / 2 + ib, [&](int64_t slot) {
+      acc += p.part[((size_t)slot * kB + (i - ib * kB)) * kB + (j - jb * kB)];
+    });
     acc *= scale;
     out[e] = acc;
     if (i != j) out[(int64_t)j * n + i] = acc;
@@ -456,20 +502,30 @@ __global__ void fx_tiles_reduce_kernel(const double* __restrict__ part, int n, i
 }
 
 struct FxPlan {
-  int nib, ntiles, splits, kblocks, kb_per, units;
+  int nib, ntiles, kblocks, grid, rounds, R, Rl;
+  int64_t units;
   size_t smem, ws_tiles, ws_sums;
 };
+
+static int64_t fx_gcd(int64_t a, int64_t b) { return b ? fx_gcd(b, a % b) : a; }
 
 FxPlan plan_fx(int64_t n, int64_t m) {
   FxPlan g{};
   g.nib = (int)((n + kB - 1) / kB);
   g.ntiles = g.nib * (g.nib + 1) / 2;
   g.kblocks = (int)((m + kCellsPerStage - 1) / kCellsPerStage);
-  const int sms = sm_count();
-  g.splits = std::max(1, std::min(g.kblocks, sms / g.ntiles));  // one wave when it fits
-  g.kb_per = (g.kblocks + g.splits - 1) / g.splits;
-  g.splits = (g.kblocks + g.kb_per - 1) / g.kb_per;               // every split non-empty
-  g.units = g.ntiles * g.splits;
+  const int64_t sms = sm_count();
+  // every SM gets the same number of units when rounds * ntiles is a
+  // multiple of the SM count; keep K windows of >= one fold window (256
+  // blocks), else fall back to about one unit per SM (split-K)
+  int64_t rounds = sms / fx_gcd(g.ntiles, sms);
+  if (g.kblocks / rounds < kFlush) rounds = std::max<int64_t>(1, sms / g.ntiles);
+  rounds = std::max<int64_t>(1, std::min<int64_t>(rounds, g.kblocks));
+  g.R = (int)((g.kblocks + rounds - 1) / rounds);
+  g.rounds = (g.kblocks + g.R - 1) / g.R;
+  g.Rl = g.kblocks - (g.rounds - 1) * g.R;
+  g.units = (int64_t)g.rounds * g.ntiles;
+  g.grid = (int)std::min<int64_t>(g.units, sms);
   g.smem = 1024 + (size_t)kStages * kStageBytes + 256;
   // the first 256 bytes of a shared workspace hold other kernels' completion
   // counters (zero between launches): partials start after them
@@ -478,16 +534,20 @@ FxPlan plan_fx(int64_t n, int64_t m) {
   return g;
 }
 
+static void fx_fill(FxParams& prm, int64_t n, const FxPlan& g) {
+  prm.n = (int)n; prm.nib = g.nib; prm.ntiles = g.ntiles; prm.kblocks = g.kblocks;
+  prm.rounds = g.rounds; prm.R = g.R; prm.Rl = g.Rl; prm.units = g.units;
+}
+
 int launch_gram_fx(const uint8_t* qd, int64_t n, const FxPlan& g, FxParams prm,
                    cudaStream_t st) {
-  prm.n = (int)n; prm.nib = g.nib; prm.ntiles = g.ntiles; prm.splits = g.splits;
-  prm.kblocks = g.kblocks; prm.kb_per = g.kb_per;
+  fx_fill(prm, n, g);
   prm.flush = kFlush;
   if (const char* e = getenv("PIDB_FX_FLUSH")) prm.flush = std::max(1, atoi(e));
   prm.noload = getenv("PIDB_FX_NOLOAD") != nullptr && atoi(getenv("PIDB_FX_NOLOAD")) != 0;
   PIDB_CUDA(cudaFuncSetAttribute(gram_fx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)g.smem));
-  gram_fx_kernel<<<g.units, kThreads, g.smem, st>>>(qd, prm);
+  gram_fx_kernel<<<g.grid, kThreads, g.smem, st>>>(qd, prm);
   PIDB_LAUNCH_CHECK("gram_fx_kernel");
   return PIDB_OK;
 }
@@ -575,7 +635,8 @@ extern "C" int pidb_gram_fixed(const uint8_t* q, int64_t n, int64_t m, double wm
   const double scale = wmax * std::ldexp(1.0, -38);
   const int64_t total = n * n;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
-  fx_tiles_reduce_kernel<<<blocks, 256, 0, st>>>(prm.part, (int)n, g.ntiles, g.splits, scale, gram);
+  fx_fill(prm, n, g);
+  fx_tiles_reduce_kernel<<<blocks, 256, 0, st>>>(prm, scale, gram);
   PIDB_LAUNCH_CHECK("fx_tiles_reduce_kernel");
   return PIDB_OK;
 }
@@ -596,8 +657,8 @@ extern "C" int pidb_gram_fixed_sums(const uint8_t* q, int64_t n, int64_t m, doub
   rc = launch_gram_fx(q, n, g, prm, st);
   if (rc != PIDB_OK) return rc;
   const double scale = wmax * std::ldexp(1.0, -38);
-  fx_sums_reduce_kernel<<<(int)((n + 127) / 128), 128, 0, st>>>(prm.part, (int)n, g.nib, g.ntiles,
-                                                               g.splits, scale, row_plain, col_inv);
+  fx_fill(prm, n, g);
+  fx_sums_reduce_kernel<<<(int)((n + 127) / 128), 128, 0, st>>>(prm, scale, row_plain, col_inv);
   PIDB_LAUNCH_CHECK("fx_sums_reduce_kernel");
   return PIDB_OK;
 }
