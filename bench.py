@@ -731,7 +731,7 @@ def run_eid_secondary(args, dev, pk):
     # DeviceEnsemble then replay a captured CUDA graph
     ms_graph = timed(lambda: pb.depth_eid(de), max(1, min(args.steps, 10)), 3, 1)
     kg, _ = kernel_ms(ev, "pidb_gram_i8")
-    km, _ = kernel_ms(ev, "pidb_member_masses")
+    kp, _ = kernel_ms(ev, "pidb_binary_pack")
     cpu = None
     if not args.no_cpu:
         U = de.values[:100, : res * res].cpu().numpy()
@@ -746,7 +746,14 @@ def run_eid_secondary(args, dev, pk):
                              "peak": INT8_TOPS_PROBE, "frac": ops / (kg * 1e-3) / 1e12 / INT8_TOPS_PROBE,
                              "kernel_ms": kg, "algorithmic_ops": ops,
                              "peak_src": "INT8 tensor peak (tcgen05 microbenchmark, profiles/r02_ubench_mma.log)"},
-           "masses_ms": km,
+           # eID is bound by max(int8 tensor time, HBM time to
+           # read the fp32 input); the input read is the floor here
+           "hbm_roofline": {"bound": "hbm", "algorithmic_bytes": n * m * 4,
+                            "floor_ms": n * m * 4 / (pk["hbm_gbs"] * 1e9) * 1e3,
+                            "frac_whole_call": n * m * 4 / (pk["hbm_gbs"] * 1e9) / (ms_graph * 1e-3),
+                            "pack_kernel_ms": kp,
+                            "pack_achieved_GBps": (n * m * 5) / (kp * 1e-3) / 1e9 if kp else None,
+                            "pack_note": "K7 reads 4 B and writes 1 B per member-voxel"},
            "ms_per_depth_graph": ms_graph}
     if cpu is not None:
         out["cpu_baseline"] = cpu
