@@ -568,6 +568,33 @@ def parity_pid_reduced(dev):
             "gram_vs_reference": _agreement(gram, ref), "gram_certifier": cert}
 
 
+def parity_eid_full(de, got):
+    """cfg2 at full size: the real reference's depth_eid and the exact-
+    summation oracle (the reference tests' ref_eid restated exactly,
+    oracle.exact.eid_fast) on the same bytes.  The GPU path is defined to be
+    bit-identical to the oracle; against depth_eid (BLAS dgemv sums) it agrees
+    to a few ulps, with ranks equal except inside exact-rational ties."""
+    fd = reference_module()
+    from oracle import exact, port
+
+    U = de.values[:, :de.m].cpu().numpy()
+    a, b, c, _ = exact.eid_fast(U)
+    out = {"size": f"{de.n} x {de.m} cells (full cfg2)",
+           "oracle_bit_identical": bool(np.array_equal(got.depth, c) and np.array_equal(got.in_in, a)
+                                        and np.array_equal(got.in_out, b)),
+           "oracle_rank_identical": bool(np.array_equal(got.rank, port.ranks(c)))}
+    if fd is not None:
+        from oracle import reference
+
+        t0 = time.perf_counter()
+        ref = fd.depth_eid(reference.from_array(fd, U, de.dims, ids=list(de.ids)),
+                           workers=os.cpu_count() or 1)
+        out["reference_seconds"] = time.perf_counter() - t0
+        out["reference"] = cpu_what()
+        out.update(_agreement(got, ref))
+    return out
+
+
 def prepare_e2e(de, world):
     """Copy the resident ensemble (this rank's slab) into pinned host memory."""
     import psutil
@@ -757,6 +784,8 @@ def run_eid_secondary(args, dev, pk):
            "ms_per_depth_graph": ms_graph}
     if cpu is not None:
         out["cpu_baseline"] = cpu
+    if not args.no_parity:
+        out["parity_full"] = parity_eid_full(de, pb.depth_eid(de))
     del de
     torch.cuda.empty_cache()
     return out
