@@ -879,3 +879,22 @@ def test_pid_gram_certified_tolerance_tiny_masses(pb, n, m, seed):
     assert np.all(np.diff(want["depth"][order]) <= 1e-12)
     if m > 1:
         np.testing.assert_array_equal(a.rank, want["rank"])
+
+
+def test_pid_gram_extreme_weights(pb):
+    """Cell weights spanning six decades: the digits carry u sqrt(w / w_max),
+    so light cells lose relative precision; the bound (A_i <= m_i /
+    sqrt(w_min w_max)) grows accordingly and the certifier resolves whatever
+    it cannot certify -- depths stay within GRAM_DEPTH_TOL, ranks exact."""
+    from paper_2512_15187_b200 import depth as D
+
+    rng = np.random.default_rng(41)
+    m = 6000
+    U = rng.uniform(size=(150, m)).astype(np.float32) ** 3
+    w = 10.0 ** rng.uniform(-3, 3, size=m)
+    e = ens(pb, U, w)
+    a = pb.depth_pid(e, algorithm="gram")
+    want = port.depth_pid(U, w)
+    close(a.depth, want["depth"], D.GRAM_DEPTH_TOL)
+    np.testing.assert_array_equal(a.rank, want["rank"])
+    print("certifier", D.LAST_GRAM_CERT)
