@@ -111,10 +111,10 @@ int pidb_member_masses(const void* u, int dtype, int64_t n, int64_t m,
  * Pack 0/1 members to u8 tiles for the integer Gram: 16 KB per (128
  * members, 128 cells), laid out [row block][cell block] in the 128-byte-
  * swizzled K-major order tcgen05 reads (line i % 128, 16-byte chunk c at
- * c ^ (i % 8)); pidb_binary_pack_bytes(n, m) bytes, 1 KB aligned, ZERO-
- * FILLED once by the caller (member rows past n, up to a multiple of 256,
- * stay zero).  Values other than 0/1 are counted in nonbinary[i] (may be
- * NULL, zero-filled by the caller) and packed as (u != 0). */
+ * c ^ (i % 8)); pidb_binary_pack_bytes(n, m) bytes, 1 KB aligned; every
+ * byte is written (member rows past n, up to a multiple of 256, as zeros).
+ * Values other than 0/1 are counted in nonbinary[i] (may be NULL, zero-
+ * filled by the caller) and packed as (u != 0). */
 size_t pidb_binary_pack_bytes(int64_t n, int64_t m);
 int pidb_binary_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
                      uint8_t* tiles, int64_t* nonbinary, void* stream);
@@ -136,8 +136,8 @@ int pidb_gram_i8(const uint8_t* tiles, int64_t n, int64_t m, int64_t* gram, void
  *
  * pidb_fixed_pack: a = u * sqrt(w / wmax) (w nullable: a = u), values in
  * [0, 1]; q = rint(a 2^31) as four base-256 digits.  Layout of q
- * (pidb_fixed_bytes(n, m) bytes, 1 KB aligned; rows past n must be zero, so
- * zero-fill it once): 16 KB tiles [ceil(n/128) row blocks][ceil(m/32) cell
+ * (pidb_fixed_bytes(n, m) bytes, 1 KB aligned; every byte is written, the
+ * padding members as zeros): 16 KB tiles [ceil(n/128) row blocks][ceil(m/32) cell
  * blocks], each 128 member lines of 128 bytes [d0 x32 | d1 x32 | d2 x32 |
  * d3 x32] in the 128-byte-swizzled K-major order of tcgen05 (16-byte chunk c
  * of line r at chunk c ^ (r % 8)).  ld % 4 == 0, u 16-byte aligned.

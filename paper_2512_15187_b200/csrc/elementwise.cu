@@ -22,17 +22,24 @@ __global__ void binary_pack_kernel(const T* __restrict__ u, int64_t n, int64_t m
                                    unsigned long long* __restrict__ nonbinary) {
   const int64_t span = nkb * 128;  // packed cells per member (zero past m)
   const int64_t segs = (span + 511) / 512;
+  // padding members up to the K2 panel height (a multiple of 256) are
+  // written as zeros: the tile buffer needs no zero fill
+  const int64_t rows = (n + 255) / 256 * 256;
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
-  for (int64_t job = wid; job < n * segs; job += nw) {
+  for (int64_t job = wid; job < rows * segs; job += nw) {
     const int64_t i = job / segs;
     const int64_t x0 = (job - i * segs) * 512 + lane * 16;
-    const T* row = u + i * ld;
+    const bool live = i < n;
+    const T* row = u + (live ? i : 0) * ld;
     unsigned long long bad = 0;
     uint32_t packed[4] = {0, 0, 0, 0};
     T vals[16];
-    if (x0 + 16 <= m) {  // 16-byte vector loads (rows are 16-byte aligned)
+    if (!live) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) vals[e] = T(0);
+    } else if (x0 + 16 <= m) {  // 16-byte vector loads (rows are 16-byte aligned)
       constexpr int PER = 16 / sizeof(T);
 #pragma unroll
       for (int k = 0; k < 16 / PER; ++k) {
@@ -60,7 +67,7 @@ __global__ void binary_pack_kernel(const T* __restrict__ u, int64_t n, int64_t m
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
-    if (lane == 0 && bad && nonbinary) atomicAdd(&nonbinary[i], bad);
+    if (lane == 0 && bad && nonbinary && live) atomicAdd(&nonbinary[i], bad);
   }
 }
 
@@ -187,7 +194,7 @@ extern "C" int pidb_binary_pack(const void* u, int dtype, int64_t n, int64_t m, 
   PIDB_REQUIRE((reinterpret_cast<uintptr_t>(tiles) & 1023) == 0, "tiles must be 1 KB aligned");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nkb = (m + 127) / 128;
-  const int64_t jobs = n * ((nkb * 128 + 511) / 512);
+  const int64_t jobs = (n + 255) / 256 * 256 * ((nkb * 128 + 511) / 512);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((jobs + 7) / 8, 148 * 16));
   if (dtype == PIDB_F32)
     binary_pack_kernel<float><<<blocks, 256, 0, st>>>(

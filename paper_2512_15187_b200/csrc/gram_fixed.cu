@@ -164,7 +164,9 @@ __global__ void __launch_bounds__(256, 3)
   __shared__ __align__(16) uint32_t stage[kPackIter][8][32];  // [block][member line][word]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane >> 3, wi = lane & 7;
-  const int64_t ngrp = (n + 7) / 8;
+  // every line of every tile is written, the padding members (rows n ..
+  // 128 ceil(n / 128) - 1) as zeros: the digit buffer needs no zero fill
+  const int64_t ngrp = (n + 127) / 128 * 16;
   for (int64_t unit = blockIdx.x; unit < ngrp * nseg; unit += gridDim.x) {
     const int64_t grp = unit / nseg, seg = unit - grp * nseg;
     const int64_t row = grp * 8 + warp;
@@ -583,7 +585,7 @@ extern "C" int pidb_fixed_pack(const void* u, int dtype, int64_t n, int64_t m, i
   double* mpart = mass ? reinterpret_cast<double*>(static_cast<char*>(ws) + 256) : nullptr;
   const int64_t nblk = (m + kCellsPerStage - 1) / kCellsPerStage;
   const int64_t nseg = (nblk + kPackSeg - 1) / kPackSeg;
-  const int64_t units = (n + 7) / 8 * nseg;
+  const int64_t units = (n + 127) / 128 * 16 * nseg;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(units, 148 * 3));
   cudaStream_t st = (cudaStream_t)stream;
   const double iw = w ? 1.0 / wmax : 1.0;

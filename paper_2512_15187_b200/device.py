@@ -203,29 +203,6 @@ class DeviceEnsemble:
             _WS[key] = ws
         return ws
 
-    def scratch(self, name: str, nbytes: int, align: int = 1024) -> torch.Tensor:
-        """A zero-filled-once, `align`-aligned uint8 buffer of this ensemble
-        (packed members: K7 tiles, K1x digit tiles), one per (name, size,
-        stream) so concurrent callers on different streams never share it.
-        Kernels that pack into it leave padding zero.  Inside a graph capture
-        the buffer is new, owned by the graph and zeroed once after the
-        capture (depth._graphed), not on every replay."""
-        capturing = torch.cuda.is_current_stream_capturing()
-        key = ("scratch", name, nbytes, torch.cuda.current_stream(self.device).cuda_stream)
-        if not capturing:
-            b = self._cache.get(key)
-            if b is not None:
-                return b
-        buf = (torch.empty if capturing else torch.zeros)(nbytes + align, dtype=torch.uint8,
-                                                         device=self.device)
-        off = (-buf.data_ptr()) % align
-        b = buf[off:off + nbytes]
-        if capturing:
-            self._cache.setdefault("graph_ws_pending", []).append(buf)
-        else:
-            self._cache[key] = b
-        return b
-
     def mean_values(self) -> torch.Tensor:
         out = torch.empty(self.m, dtype=torch.float64, device=self.device)
         N.call("pidb_mean_mask", self.ptr(), self.dtype_code, self.n, self.m, self.ld,

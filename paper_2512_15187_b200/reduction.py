@@ -34,6 +34,13 @@ def _allreduce(t: torch.Tensor, de: DeviceEnsemble) -> None:
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=de.process_group)
 
 
+def _aligned_bytes(nbytes: int, dev, align: int = 1024) -> torch.Tensor:
+    """Uninitialised `align`-aligned uint8 device buffer (caching allocator)."""
+    buf = torch.empty(nbytes + align, dtype=torch.uint8, device=dev)
+    off = (-buf.data_ptr()) % align
+    return buf[off:off + nbytes]
+
+
 def pack_fixed(de: DeviceEnsemble, soft: torch.Tensor | None = None,
                mass: torch.Tensor | None = None):
     """K1x pack: members -> fixed-point digit tiles for the int8 Gram
@@ -43,7 +50,7 @@ def pack_fixed(de: DeviceEnsemble, soft: torch.Tensor | None = None,
     the same pass.  The digit buffer (zero-filled once: rows
     past n stay zero) is kept on the ensemble and re-packed on every call
     (the members may change in place)."""
-    q = de.scratch("k1x_digits", int(N.load().pidb_fixed_bytes(de.n, de.m)))
+    q = _aligned_bytes(int(N.load().pidb_fixed_bytes(de.n, de.m)), de.device)
     wmax = de._cache.get("fixed_wmax")
     if wmax is None:
         wmax = float(de.weights.max()) if de.weights is not None else 1.0
@@ -80,9 +87,10 @@ def gram_device(de: DeviceEnsemble) -> torch.Tensor:
 def pack_binary(de: DeviceEnsemble, nonbinary: torch.Tensor | None = None) -> torch.Tensor:
     """K7: 0/1 members -> u8 tiles for K2 (include/pidb.h); optionally counts
     each member's values that are neither 0 nor 1 (`nonbinary`, int64 (n,)
-    zero-filled by the caller).  The tile buffer is zero-filled once (padding
-    rows stay zero) and kept on the ensemble; it is re-packed on every call."""
-    b = de.scratch("k7_tiles", int(N.load().pidb_binary_pack_bytes(de.n, de.m)))
+    zero-filled by the caller).  The tile buffer comes from the stream-aware
+    caching allocator per call (the pack writes every byte, padding included;
+    inside a graph capture it becomes the graph's own)."""
+    b = _aligned_bytes(int(N.load().pidb_binary_pack_bytes(de.n, de.m)), de.device)
     from .depth import _launch
 
     _launch("pidb_binary_pack", de.ptr(), de.dtype_code, de.n, de.m, de.ld, b.data_ptr(),
