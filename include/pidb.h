@@ -108,7 +108,9 @@ int pidb_member_masses(const void* u, int dtype, int64_t n, int64_t m,
                        void* stream);
 
 /* ---------------------------------------------------------------- K7 ----
- * Pack 0/1 members to u8 tiles for the integer Gram: 16 KB per (128
+ * Binary check + pack (member_masses(require_binary=True) depth.py:94-100,
+ * ProbMask.is_binary grid.py:125-127) of 0/1 members to u8 tiles for the
+ * integer Gram: 16 KB per (128
  * members, 128 cells), laid out [row block][cell block] in the 128-byte-
  * swizzled K-major order tcgen05 reads (line i % 128, 16-byte chunk c at
  * c ^ (i % 8)); pidb_binary_pack_bytes(n, m) bytes, 1 KB aligned; every
@@ -235,7 +237,9 @@ int pidb_copy_rows(void* dst, int64_t dst_pitch_bytes, const void* src,
                    void* stream);
 
 /* dst[j] = sum_k src[k*len + j] for k = 0..rows-1 in ascending order: the
- * fixed-order combination of per-slab partial sums (streamed PID-mean). */
+ * fixed-order combination of per-slab partial sums (the streamed PID-mean of
+ * a host-resident ensemble, depth_pid_mean depth.py:246-287 with the chunk
+ * order of reduction.py:30-33 generalised to cell slabs). */
 int pidb_sum_rows(const double* src, int64_t rows, int64_t len, double* dst, void* stream);
 
 /* One-pass value check of raw member data (ProbMask policy, grid.py:105-116):
