@@ -18,6 +18,9 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpidb.so"
 BUILD = ROOT / "build" / "pidb"
+# checked build: device-side bounds asserts (PIDB_DCHECK), loaded via PIDB_LIB
+LIB_CHECKED = PKG / "libpidb_checked.so"
+BUILD_CHECKED = ROOT / "build" / "pidb_checked"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
@@ -51,36 +54,38 @@ def _needs_rebuild(obj: Path, src: Path) -> bool:
     return any(d.stat().st_mtime > t for d in deps if d.exists())
 
 
-def _compile(src: Path) -> tuple[Path, str]:
-    obj = BUILD / (src.stem + ".o")
+def _compile(src: Path, checked: bool = False) -> tuple[Path, str]:
+    obj = (BUILD_CHECKED if checked else BUILD) / (src.stem + ".o")
     if not _needs_rebuild(obj, src):
         return obj, ""
-    cmd = [nvcc(), *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DPIDB_DEVICE_CHECKS"] if checked else []), "-c", str(src),
+           "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr}")
     return obj, r.stderr
 
 
-def build(verbose: bool = False) -> Path:
-    BUILD.mkdir(parents=True, exist_ok=True)
+def build(verbose: bool = False, checked: bool = False) -> Path:
+    out_dir, lib = (BUILD_CHECKED, LIB_CHECKED) if checked else (BUILD, LIB)
+    out_dir.mkdir(parents=True, exist_ok=True)
     srcs = sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        results = list(ex.map(_compile, srcs))
+        results = list(ex.map(lambda s: _compile(s, checked), srcs))
     objs = [o for o, _ in results]
     if verbose:
         for _, log in results:
             if log:
                 sys.stderr.write(log)
-    if not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
-        tmp = LIB.with_suffix(".so.tmp")
+    if not lib.exists() or any(o.stat().st_mtime > lib.stat().st_mtime for o in objs):
+        tmp = lib.with_suffix(".so.tmp")
         cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, checked="--checked" in sys.argv))

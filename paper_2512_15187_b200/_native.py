@@ -8,12 +8,15 @@ raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 from .errors import ValidationError
 
-LIB_PATH = Path(__file__).resolve().parent / "libpidb.so"
+# PIDB_LIB selects another build of the same ABI (e.g. libpidb_checked.so,
+# the device-bounds-checked build of tools/checked_sweep.sh)
+LIB_PATH = Path(os.environ.get("PIDB_LIB") or Path(__file__).resolve().parent / "libpidb.so")
 
 PIDB_OK = 0
 PIDB_EINVAL = -1

@@ -37,6 +37,25 @@ int encode_tma_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Device-side bounds checks, compiled only into the checked build
+// (python -m paper_2512_15187_b200._build --checked -> libpidb_checked.so,
+// loaded with PIDB_LIB): the substitute for compute-sanitizer memcheck, which
+// the GPU pool refuses.  A failed check prints the site and traps.
+#ifdef PIDB_DEVICE_CHECKS
+#define PIDB_DCHECK(cond, what)                                                        \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("pidb device check failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define PIDB_DCHECK(cond, what) \
+  do {                          \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------- device ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

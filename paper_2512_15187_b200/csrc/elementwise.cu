@@ -63,6 +63,7 @@ __global__ void binary_pack_kernel(const T* __restrict__ u, int64_t n, int64_t m
       const int c = (int)((x0 & 127) >> 4);
       uint8_t* dst = tiles + ((i >> 7) * nkb + (x0 >> 7)) * (int64_t)16384 + r * 128 +
                      (((c ^ r) & 7) << 4);
+      PIDB_DCHECK((i >> 7) < 2 * ((n + 255) / 256) && (x0 >> 7) < nkb, "K7 tile bounds");
       *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
     }
 #pragma unroll

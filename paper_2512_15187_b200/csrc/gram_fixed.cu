@@ -237,9 +237,11 @@ __global__ void __launch_bounds__(256, 3)
 #pragma unroll
       for (int t = threadIdx.x; t < kPackIter * 64; t += 256) {
         const int blk_t = t >> 6, off = (t & 63) * 16;
-        if (b + blk_t < b1)
+        if (b + blk_t < b1) {
+          PIDB_DCHECK(grp / 16 < (n + 127) / 128 && b + blk_t < nblk, "K1x pack tile bounds");
           *reinterpret_cast<uint4*>(atom0 + (b + blk_t) * (int64_t)kTileBytes + off) =
               reinterpret_cast<const uint4*>(&stage[blk_t][0][0])[t & 63];
+        }
       }
       __syncthreads();
     }
@@ -247,6 +249,7 @@ __global__ void __launch_bounds__(256, 3)
     if (soft && live && lane == 0 && cnt) atomicAdd(soft + row, (unsigned long long)cnt);
     if (mpart) {
       mass = warp_sum(mass);
+      PIDB_DCHECK(!live || (row < n && seg < nseg), "K1x pack mass partial bounds");
       if (live && lane == 0) mpart[row * nseg + seg] = mass;
     }
   }
@@ -322,6 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             mbar_arrive_expect_tx(&full[s], bytes);
             const int64_t kb = kb0 + k;
+            PIDB_DCHECK(kb < p.kblocks && ib < p.nib && jb < p.nib, "K1x operand tile bounds");
             bulk_load(a, qd + ((int64_t)ib * p.kblocks + kb) * kTileBytes, kTileBytes, &full[s],
                       pol);
             if (!diag)
@@ -417,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int e = 0; e < 32; ++e) tile[row * kLd + c0 + e] = acc[e];
       epi_sync();
       const int64_t slot = u;
+      PIDB_DCHECK(slot < p.units && t < p.ntiles, "K1x output slot bounds");
       if (!p.sums) {
         double* dst = p.part + (size_t)slot * kB * kB;
         for (int e = et; e < kB * kB; e += kEpiWarps * 32) dst[e] = tile[(e / kB) * kLd + (e % kB)];

@@ -87,6 +87,9 @@ __global__ void __launch_bounds__(kGramThreads, 1)
         unsigned char* a = ring + s * kStageBytes;
         mbar_arrive_expect_tx(&full[s], kStageBytes);
         const int64_t kb = kb0 + k;  // three contiguous 16 KB tiles: A, then B's two halves
+        PIDB_DCHECK(kb < p.kblocks && ib < 2 * ((p.n + 255) / 256) &&
+                        2 * jb + 1 < 2 * ((p.n + 255) / 256),
+                    "K2 operand tile bounds");
         bulk_load(a, tiles + ((int64_t)ib * p.kblocks + kb) * kABytes, kABytes, &full[s], pol);
         bulk_load(a + kABytes, tiles + ((int64_t)(2 * jb) * p.kblocks + kb) * kABytes, kABytes,
                   &full[s], pol);
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(kGramThreads, 1)
     const int row = quad * 32 + lane;
     mbar_wait(tmem_full, 0);
     tc::fence_after();
+    PIDB_DCHECK(unit < p.ntiles * p.splits, "K2 partial bounds");
     int32_t* dst = p.part + ((size_t)unit * kBM + row) * kBN;
 #pragma unroll 1
     for (int c = 0; c < kBN; c += 32) {

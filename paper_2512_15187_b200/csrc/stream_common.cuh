@@ -521,6 +521,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       const double a = warp_sum(acc_row[k]);
       const double c = warp_sum(acc_mass[k]);
       if (lane == 0 && rl < nloc) {
+        PIDB_DCHECK(r0 + rl < n && cid < p.groups, "K5 row partial bounds");
         double* dst = p.part + part_at(p, 1, 0, r0 + rl, cid) * 2;
         dst[0] = a;
         dst[1] = c;
