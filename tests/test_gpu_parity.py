@@ -625,6 +625,8 @@ def test_graph_replay_matches_eager(pb, monkeypatch):
     matrix, so in-place updates are seen."""
     from paper_2512_15187_b200 import depth as D
 
+    if not D._GRAPHS:
+        pytest.skip("CUDA graphs disabled (PIDB_GRAPHS=0)")
     rng = np.random.default_rng(12)
     U = rng.uniform(size=(37, 3000)).astype(np.float32)
     B = (rng.uniform(size=(29, 2500)) < 0.4).astype(np.float32)

@@ -10,9 +10,9 @@
 set -u
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-export PIDB_LIB="$PWD/paper_2512_15187_b200/libpidb_checked.so" CUDA_LAUNCH_BLOCKING=1 PIDB_GRAPHS=0
+export PIDB_LIB="$PWD/paper_2512_15187_b200/libpidb_checked.so" CUDA_LAUNCH_BLOCKING=1
 test -f "$PIDB_LIB" || { echo "missing $PIDB_LIB"; exit 2; }
-timeout 1200 python tools/sweep_cases.py > gpurun_out/checked_sweep.log 2>&1
+PIDB_GRAPHS=0 timeout 1200 python tools/sweep_cases.py > gpurun_out/checked_sweep.log 2>&1
 echo "sweep rc=$? $(grep -c 'device check failed' gpurun_out/checked_sweep.log) failed checks"
 timeout 1800 python -m pytest tests/test_gpu_parity.py tests/test_gpu_headline.py -q -x \
     -p no:cacheprovider > gpurun_out/checked_pytest.log 2>&1
