@@ -116,7 +116,8 @@ struct Vec4;
 template <>
 struct Vec4<float> {
   float4 v;
-  __device__ __forceinline__ double operator[](int e) const {
+  __device__ __forceinline__ double operator[](int e) const { return (double)f(e); }
+  __device__ __forceinline__ float f(int e) const {
     return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
   }
 };
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(256, 3)
             // unweighted fp32: u 2^31 is exact in fp32, so is its rounding
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float f = (float)v[j][e];
+              const float f = v[j].f(e);
               mass += (double)f;
               qv[e] = min(__float2uint_rn(f * 2147483648.0f), 0x80000000u);
             }
