@@ -156,8 +156,8 @@ __device__ __forceinline__ Vec4<T> fx_load4(const T* __restrict__ src, int64_t x
 constexpr int kPackSeg = 128;   // cell blocks per CTA unit
 constexpr int kPackIter = 16;   // cell blocks per CTA iteration (4 loads in flight per lane)
 
-template <typename T>
-__global__ void __launch_bounds__(256, 3)
+template <typename T, bool W>
+__global__ void __launch_bounds__(256, (sizeof(T) == 4 && !W) ? 4 : 3)
     fx_pack_kernel(const T* __restrict__ u, int64_t ld, int n, int64_t m,
                    const double* __restrict__ w, double inv_wmax, uint8_t* __restrict__ q,
                    int64_t nblk, int64_t nseg, unsigned long long* __restrict__ soft,
@@ -191,8 +191,8 @@ __global__ void __launch_bounds__(256, 3)
       for (int j = 0; j < kPackIter / 4; ++j) {
         const int64_t x = (b + 4 * j + sub) * kCellsPerStage + 4 * wi;
         uint32_t qv[4];
-        if constexpr (sizeof(T) == 4) {
-          if (!w) {
+        if constexpr (sizeof(T) == 4 && !W) {
+          {
             // unweighted fp32: u 2^31 is exact in fp32, so is its rounding
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -202,11 +202,11 @@ __global__ void __launch_bounds__(256, 3)
             }
           }
         }
-        if (sizeof(T) != 4 || w) {
+        if constexpr (sizeof(T) != 4 || W) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             double a = v[j][e];
-            if (w && x + e < m) {
+            if (W && x + e < m) {
               const double wx = __ldcs(w + x + e);
               mass = fma(wx, a, mass);
               a *= sqrt(wx * inv_wmax);
@@ -595,16 +595,20 @@ extern "C" int pidb_fixed_pack(const void* u, int dtype, int64_t n, int64_t m, i
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(units, 148 * 3));
   cudaStream_t st = (cudaStream_t)stream;
   const double iw = w ? 1.0 / wmax : 1.0;
-  if (dtype == PIDB_F32)
-    fx_pack_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(u), ld, (int)n, m, w,
-                                                  iw, q, nblk, nseg,
-                                                  reinterpret_cast<unsigned long long*>(soft_count),
-                                                  mpart);
+  unsigned long long* sc = reinterpret_cast<unsigned long long*>(soft_count);
+  const int b4 = (int)std::max<int64_t>(1, std::min<int64_t>(units, 148 * 4));
+  if (dtype == PIDB_F32 && !w)  // register-light variant: 4 CTAs per SM
+    fx_pack_kernel<float, false><<<b4, 256, 0, st>>>(static_cast<const float*>(u), ld, (int)n, m,
+                                                     w, iw, q, nblk, nseg, sc, mpart);
+  else if (dtype == PIDB_F32)
+    fx_pack_kernel<float, true><<<blocks, 256, 0, st>>>(static_cast<const float*>(u), ld, (int)n,
+                                                        m, w, iw, q, nblk, nseg, sc, mpart);
+  else if (!w)
+    fx_pack_kernel<double, false><<<blocks, 256, 0, st>>>(static_cast<const double*>(u), ld,
+                                                          (int)n, m, w, iw, q, nblk, nseg, sc, mpart);
   else
-    fx_pack_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(u), ld, (int)n, m, w,
-                                                   iw, q, nblk, nseg,
-                                                   reinterpret_cast<unsigned long long*>(soft_count),
-                                                   mpart);
+    fx_pack_kernel<double, true><<<blocks, 256, 0, st>>>(static_cast<const double*>(u), ld, (int)n,
+                                                         m, w, iw, q, nblk, nseg, sc, mpart);
   PIDB_LAUNCH_CHECK("fx_pack_kernel");
   if (mass) {
     fx_mass_reduce_kernel<<<(int)((n + 7) / 8), 256, 0, st>>>(mpart, (int)n, nseg, mass);
