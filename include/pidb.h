@@ -154,8 +154,8 @@ int pidb_fixed_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
                     const double* w, double wmax, uint8_t* q, uint64_t* soft_count,
                     double* mass, void* ws, size_t ws_bytes, void* stream);
 /* G[i*n+j] = wmax * 2^-62 * sum_x (digit-pair levels 0..3 of q_i q_j): every
- * product accumulates exactly (int32 TMEM, folded into fp64 every 8192
- * cells); |G - G_exact| <= wmax (2^-32 (A_i + A_j) + m 2^-64 +
+ * product accumulates exactly (32-bit TMEM read as uint32, folded into fp64
+ * every 16384 cells); |G - G_exact| <= wmax (2^-32 (A_i + A_j) + m 2^-64 +
  * 2.78e-9 min(soft_i, soft_j)), A = sum_x a (DESIGN.md §3 K1).
  * `sums` selects the workspace of pidb_gram_fixed_sums (1) or of the full
  * Gram (0). */

@@ -26,9 +26,9 @@
 // d_k e_l; the levels s = 0..3 (10 digit pairs) are kept, the dropped
 // levels 4..6 are < 2.8e-9 per cell product and zero whenever either value
 // has no low-order digits (0, 1 and every value that quantises to a
-// multiple of 2^-7).  Each level accumulates in its own int32 TMEM
-// accumulator (M = N = 128, 4 x 128 = all 512 columns) -- exact for 256
-// stages (8192 cells; worst case 1.6e9 < 2^31) -- then the epilogue warps
+// multiple of 2^-7).  Each level accumulates in its own 32-bit TMEM
+// accumulator (M = N = 128, 4 x 128 = all 512 columns) -- exact, read as
+// uint32, for 512 stages (16384 cells; worst case 3.2e9 < 2^32) -- then the epilogue warps
 // fold v = ((L0*256 + L1)*256 + L2)*256 + L3 (an integer < 2^53, exact in fp64) into fp64
 // accumulators held in registers.  Emulated against the fp64 Gram
 // (tools/fixed_gram_emulation.py): depth error <= 3.2e-9 at N = 300 with
@@ -56,7 +56,11 @@ constexpr int kCellsPerStage = 32;
 constexpr int kStages = 6;                   // 192 KB ring (also holds the 132 KB fp64 tile at the end)
 constexpr int kTileBytes = kB * kLine;       // 16 KB
 constexpr int kStageBytes = 2 * kTileBytes;  // A and B
-constexpr int kFlush = 256;                  // stages per int32 accumulation window
+// stages per 32-bit accumulation window: the level sums are non-negative and
+// integer MMA accumulation wraps modulo 2^32, so read as uint32 they are exact
+// below 2^32 -- 512 stages (16384 cells; worst case 3.2e9) -- half the folds
+// of a signed 2^31 bound
+constexpr int kFlush = 512;
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = (2 + kEpiWarps) * 32;
 constexpr uint32_t kIdesc = tc::idesc(tc::kCS32, tc::kU8, kB, kB);
@@ -403,9 +407,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            double v = (double)(int32_t)r[0][e];
+            double v = (double)r[0][e];  // uint32 (see kFlush)
 #pragma unroll
-            for (int lv = 1; lv < 4; ++lv) v = fma(v, 256.0, (double)(int32_t)r[lv][e]);
+            for (int lv = 1; lv < 4; ++lv) v = fma(v, 256.0, (double)r[lv][e]);
             acc[4 * h + e] += v;
           }
         }

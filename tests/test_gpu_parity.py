@@ -900,3 +900,23 @@ def test_pid_gram_extreme_weights(pb):
     close(a.depth, want["depth"], D.GRAM_DEPTH_TOL)
     np.testing.assert_array_equal(a.rank, want["rank"])
     print("certifier", D.LAST_GRAM_CERT)
+
+
+def test_fixed_gram_full_window_near_one(pb):
+    """Members of values just below 1 (digits 127, 255, 255, 255): one
+    512-stage window sums 3.2e9 > 2^31 in the level-3 accumulator, which is
+    exact only read as uint32 (the integer MMA wraps modulo 2^32).  Checked
+    against the exact fp64 Gram of the quantised values."""
+    from paper_2512_15187_b200.reduction import gram_device
+
+    n, m = 5, 16384 * 2 + 100
+    U = np.full((n, m), np.float32(1.0) - np.float32(2.0 ** -24), dtype=np.float32)
+    U[1] = 0.5
+    U[3, ::3] = 0.25
+    de = pb.DeviceEnsemble.from_tensor(torch.from_numpy(U))
+    got = gram_device(de).cpu().numpy()
+    X = U.astype(np.float64)
+    want = X @ X.T
+    err = np.abs(got - want) / want
+    print("max rel err", err.max())
+    assert err.max() < 1e-8
