@@ -498,7 +498,8 @@ def run_ours(args, rank, world, local, pg):
     del de
     torch.cuda.empty_cache()
     if not args.no_e2e:
-        line["e2e"] = run_e2e(args, host, e2e_meta, meta, fn, world, pg, dev) if host is not None \
+        line["e2e"] = run_e2e(args, host, e2e_meta, meta, fn, world, pg, dev,
+                              res_chk if world == 1 else None) if host is not None \
             else e2e_meta
         del host
 
@@ -626,7 +627,7 @@ def prepare_e2e(de, world):
     return host, None
 
 
-def run_e2e(args, host, _, meta, fn, world, pg, dev):
+def run_e2e(args, host, _, meta, fn, world, pg, dev, resident=None):
     """The public API on this rank's pinned host tensor.  Single GPU, PID-mean:
     ``depth_pid_mean(host_tensor)`` streams cell slabs through HBM (H2D on a
     side stream overlapped with in-place validation and K5).  Otherwise the
@@ -645,6 +646,11 @@ def run_e2e(args, host, _, meta, fn, world, pg, dev):
         return fn(e)
 
     ms = timed(step, E2E_STEPS, 3, world)
+    check = None
+    if resident is not None:  # the host path must give the resident path's depths
+        r = step()
+        check = {"max_abs_depth_diff_vs_resident": float(np.abs(r.depth - resident.depth).max()),
+                 "ranks_equal_resident": bool(np.array_equal(r.rank, resident.rank))}
     total = n * int(np.prod(dims))
     path = ("depth_pid_mean(pinned host tensor): cell slabs of "
             f"{D.STREAM_SLAB_BYTES >> 20} MB, H2D on a side stream overlapped with in-place "
@@ -656,7 +662,7 @@ def run_e2e(args, host, _, meta, fn, world, pg, dev):
             "steps": E2E_STEPS, "warmup": 3,
             "h2d_bytes_per_step": n * m * 4, "d2h_bytes_per_step": (5 * n + n + 1) * 8,
             "h2d_GBps_effective": n * m * 4 / (ms * 1e-3) / 1e9,
-            "bound": "PCIe host-to-device copy", "path": path}
+            "bound": "PCIe host-to-device copy", "path": path, "check": check}
 
 
 # cuBLAS TF32 / INT8 dense GEMM peaks measured on this pool's B200 by
