@@ -28,19 +28,20 @@
 // has no low-order digits (0, 1 and every value that quantises to a
 // multiple of 2^-7).  Each level accumulates in its own 32-bit TMEM
 // accumulator (M = N = 128, 4 x 128 = all 512 columns) -- exact, read as
-// uint32, for 512 stages (16384 cells; worst case 3.2e9 < 2^32) -- then the epilogue warps
-// fold v = ((L0*256 + L1)*256 + L2)*256 + L3 (an integer < 2^53, exact in fp64) into fp64
-// accumulators held in registers.  Emulated against the fp64 Gram
+// uint32, for 512 stages (16384 cells; worst case 3.2e9 < 2^32) -- then
+// the epilogue warps fold v = ((L0*256 + L1)*256 + L2)*256 + L3 (an integer
+// < 2^53, exact in fp64) into fp64 accumulators held in registers.
+// Emulated against the fp64 Gram before it was built
 // (tools/fixed_gram_emulation.py): depth error <= 3.2e-9 at N = 300 with
 // uniform, u^8 and ellipsoid members, 0 rank swaps.
 //
 // Work: 128 x 128 tiles of the upper block triangle x K rounds, persistent
 // CTAs over the (round, tile) units (all 148 SMs busy with equal work where
-// the counts allow); diagonal tiles load one operand.  Warps (576 threads): 0 TMA producer
-// (6-stage ring, 32 KB per stage), 1 MMA issuer, 2-17 epilogue (TMEM lane
-// quadrant = warp % 4, 32 columns each).  Outputs per (tile, split) unit:
-// the fp64 tile, or (PID) its row sums, inverse-mass-weighted row sums and
-// the two column counterparts; fixed-order reductions finish both.
+// the counts allow); diagonal tiles load one operand.  Warps (576 threads):
+// 0 bulk-copy producer (6-stage ring, 32 KB per stage), 1 MMA issuer, 2-17
+// epilogue (TMEM lane quadrant = warp % 4, 32 columns each).  Outputs per
+// unit: the fp64 tile, or (PID) its row sums, inverse-mass-weighted row sums
+// and the two column counterparts; fixed-order reductions finish both.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
