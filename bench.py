@@ -120,7 +120,7 @@ def dist_setup():
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if os.environ.get("PIDB_BENCH_SHARE_GPU") == "1":
-            # flow check only (tools/dist_check.sh): every rank on cuda:0, gloo
+            # flow check only (as tools/dist_check.py does): every rank on cuda:0, gloo
             # collectives; the timings of such a run mean nothing
             local = 0
             torch.cuda.set_device(0)

@@ -174,7 +174,7 @@ int pidb_gram_fixed_sums(const uint8_t* q, int64_t n, int64_t m, double wmax,
  *   out[i*nc+j] = sum_x w(x) rows[i,x] * c(j,x),  c = cols or 1 - cols
  * rows (nr, ldr) and cols (nc, ldc) of dtype PIDB_F32 or PIDB_F64 (both the
  * same), w nullable; fp64 products and sums (the reference's contract, its
- * tests use rtol 1e-12, tests/test_reduction.py:46-66).  Deterministic
+ * tests use rtol 1e-12, /root/reference/pkg/tests/test_reduction.py:46-66).  Deterministic
  * split-K with a fixed-order reduction; workspace needs no initialisation. */
 size_t pidb_gram_f64_workspace_bytes(int64_t nr, int64_t nc, int64_t m);
 int pidb_gram_f64(const void* rows, const void* cols, int dtype, int64_t nr,
