@@ -802,10 +802,34 @@ def run_eid_secondary(args, dev, pk):
                             "pack_achieved_GBps": (n * m * 5) / (kp * 1e-3) / 1e9 if kp else None,
                             "pack_note": "K7 reads 4 B and writes 1 B per member-voxel"},
            "ms_per_depth_graph": ms_graph}
+    # the same members held as bytes (a bool ensemble): K2 loads them by TMA,
+    # no pack pass; the input floor drops to 1 B per member-voxel
+    ref = pb.depth_eid(de)
+    db = pb.stage(de.values[:, :m] != 0)
+    D.KERNEL_EVENTS = []
+    rb = pb.depth_eid(db)
+    D.KERNEL_EVENTS = []
+    ms_b = timed(lambda: pb.depth_eid(db), max(1, min(args.steps, 10)), 3, 1)
+    evb = D.KERNEL_EVENTS
+    D.KERNEL_EVENTS = None
+    ms_bg = timed(lambda: pb.depth_eid(db), max(1, min(args.steps, 10)), 3, 1)
+    kb, _ = kernel_ms(evb, "pidb_gram_i8_bytes")
+    out["byte_ensemble"] = {
+        "input": "the cfg2 members as a bool tensor (1 B per member-voxel), pb.stage(bool)",
+        "ms_per_depth": ms_b, "ms_per_depth_graph": ms_bg,
+        "value": n * m / (ms_bg * 1e-3), "unit": "member-voxels/s",
+        "gram_kernel_ms": kb,
+        "gram_frac_of_int8_peak": ops / (kb * 1e-3) / 1e12 / INT8_TOPS_PROBE if kb else None,
+        "hbm_floor_ms": n * m / (pk["hbm_gbs"] * 1e9) * 1e3,
+        "bit_identical_to_fp32_path": bool(np.array_equal(rb.depth, ref.depth)
+                                           and np.array_equal(rb.in_in, ref.in_in)
+                                           and np.array_equal(rb.in_out, ref.in_out)
+                                           and np.array_equal(rb.rank, ref.rank))}
+    del db
     if cpu is not None:
         out["cpu_baseline"] = cpu
     if not args.no_parity:
-        out["parity_full"] = _guarded("cfg2 parity", parity_eid_full, de, pb.depth_eid(de))
+        out["parity_full"] = _guarded("cfg2 parity", parity_eid_full, de, ref)
     del de
     torch.cuda.empty_cache()
     return out

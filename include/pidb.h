@@ -48,7 +48,9 @@ enum pidb_status {
   PIDB_EWORKSPACE = -4   /* workspace too small                                */
 };
 
-enum pidb_dtype { PIDB_F32 = 0, PIDB_F64 = 1 };
+/* PIDB_U8: 0/1 members stored one byte per cell (a binary ensemble); taken
+ * by pidb_binary_pack (check / pack) and pidb_gram_i8_bytes only. */
+enum pidb_dtype { PIDB_F32 = 0, PIDB_F64 = 1, PIDB_U8 = 2 };
 
 /* Epilogue modes for pidb_depth_epilogue. */
 enum pidb_epilogue_mode {
@@ -116,7 +118,9 @@ int pidb_member_masses(const void* u, int dtype, int64_t n, int64_t m,
  * c ^ (i % 8)); pidb_binary_pack_bytes(n, m) bytes, 1 KB aligned; every
  * byte is written (member rows past n, up to a multiple of 256, as zeros).
  * Values other than 0/1 are counted in nonbinary[i] (may be NULL, zero-
- * filled by the caller) and packed as (u != 0). */
+ * filled by the caller) and packed as (u != 0).  dtype PIDB_F32, PIDB_F64
+ * or PIDB_U8 (16-byte aligned rows); tiles == NULL only counts (the binary
+ * check of a byte ensemble, BinaryMask.__post_init__ grid.py:145-148). */
 size_t pidb_binary_pack_bytes(int64_t n, int64_t m);
 int pidb_binary_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
                      uint8_t* tiles, int64_t* nonbinary, void* stream);
@@ -130,6 +134,13 @@ int pidb_binary_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
 size_t pidb_gram_i8_workspace_bytes(int64_t n, int64_t m);
 int pidb_gram_i8(const uint8_t* tiles, int64_t n, int64_t m, int64_t* gram, void* ws,
                  size_t ws_bytes, void* stream);
+/* Same Gram straight from a byte ensemble (PIDB_U8 members, row pitch ld
+ * bytes, base and ld 16-byte aligned): the operand boxes are 2D TMA loads
+ * with 128-byte swizzle from the member matrix itself, no pack pass.  Values
+ * must be 0/1 (checked once when the ensemble is staged).  Workspace as
+ * pidb_gram_i8_workspace_bytes(n, m). */
+int pidb_gram_i8_bytes(const uint8_t* u, int64_t n, int64_t m, int64_t ld, int64_t* gram,
+                       void* ws, size_t ws_bytes, void* stream);
 
 /* --------------------------------------------------------------- K1x ----
  * Fixed-point Gram on the int8 tensor cores with exact integer accumulation

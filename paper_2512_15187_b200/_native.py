@@ -26,6 +26,7 @@ PIDB_EWORKSPACE = -4
 
 PIDB_F32 = 0
 PIDB_F64 = 1
+PIDB_U8 = 2
 PIDB_EPI_PID_MEAN = 0
 PIDB_EPI_PID = 1
 PIDB_EPI_DICE = 2
@@ -58,6 +59,7 @@ SIGNATURES: dict[str, tuple] = {
     "pidb_binary_pack": (_int, [_p, _int, _i64, _i64, _i64, _p, _p, _p]),
     "pidb_gram_i8_workspace_bytes": (_sz, [_i64, _i64]),
     "pidb_gram_i8": (_int, [_p, _i64, _i64, _p, _p, _sz, _p]),
+    "pidb_gram_i8_bytes": (_int, [_p, _i64, _i64, _i64, _p, _p, _sz, _p]),
     "pidb_gram_reduce": (_int, [_p, _i64, _p, _p, _p, _p]),
     "pidb_fixed_bytes": (_sz, [_i64, _i64]),
     "pidb_fixed_pack_workspace_bytes": (_sz, [_i64, _i64]),

@@ -24,7 +24,7 @@ __global__ void binary_pack_kernel(const T* __restrict__ u, int64_t n, int64_t m
   const int64_t segs = (span + 511) / 512;
   // padding members up to the K2 panel height (a multiple of 256) are
   // written as zeros: the tile buffer needs no zero fill
-  const int64_t rows = (n + 255) / 256 * 256;
+  const int64_t rows = tiles ? (n + 255) / 256 * 256 : n;  // NULL tiles: count only
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
@@ -58,7 +58,7 @@ __global__ void binary_pack_kernel(const T* __restrict__ u, int64_t n, int64_t m
       bad += !(v == T(0) || v == T(1));
       packed[e >> 2] |= (uint32_t)(v != T(0)) << (8 * (e & 3));
     }
-    if (x0 < span) {
+    if (tiles && x0 < span) {
       const int r = (int)(i & 127);
       const int c = (int)((x0 & 127) >> 4);
       uint8_t* dst = tiles + ((i >> 7) * nkb + (x0 >> 7)) * (int64_t)16384 + r * 128 +
@@ -191,11 +191,14 @@ extern "C" size_t pidb_binary_pack_bytes(int64_t n, int64_t m) {
 
 extern "C" int pidb_binary_pack(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
                                 uint8_t* tiles, int64_t* nonbinary, void* stream) {
-  PIDB_REQUIRE(u && tiles && n >= 1 && m >= 1 && ld >= m, "bad arguments to pidb_binary_pack");
+  PIDB_REQUIRE(u && (tiles || nonbinary) && n >= 1 && m >= 1 && ld >= m,
+               "bad arguments to pidb_binary_pack");
   PIDB_REQUIRE((reinterpret_cast<uintptr_t>(tiles) & 1023) == 0, "tiles must be 1 KB aligned");
+  PIDB_REQUIRE(dtype != PIDB_U8 || ((reinterpret_cast<uintptr_t>(u) & 15) == 0 && ld % 16 == 0),
+               "byte members need a 16-byte aligned base and row pitch");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nkb = (m + 127) / 128;
-  const int64_t jobs = (n + 255) / 256 * 256 * ((nkb * 128 + 511) / 512);
+  const int64_t jobs = (tiles ? (n + 255) / 256 * 256 : n) * ((nkb * 128 + 511) / 512);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((jobs + 7) / 8, 148 * 16));
   if (dtype == PIDB_F32)
     binary_pack_kernel<float><<<blocks, 256, 0, st>>>(
@@ -205,8 +208,12 @@ extern "C" int pidb_binary_pack(const void* u, int dtype, int64_t n, int64_t m, 
     binary_pack_kernel<double><<<blocks, 256, 0, st>>>(
         static_cast<const double*>(u), n, m, ld, tiles, nkb,
         reinterpret_cast<unsigned long long*>(nonbinary));
+  else if (dtype == PIDB_U8)
+    binary_pack_kernel<uint8_t><<<blocks, 256, 0, st>>>(
+        static_cast<const uint8_t*>(u), n, m, ld, tiles, nkb,
+        reinterpret_cast<unsigned long long*>(nonbinary));
   else
-    PIDB_REQUIRE(false, "dtype must be PIDB_F32 or PIDB_F64");
+    PIDB_REQUIRE(false, "dtype must be PIDB_F32, PIDB_F64 or PIDB_U8");
   PIDB_LAUNCH_CHECK("binary_pack_kernel");
   return PIDB_OK;
 }
@@ -215,6 +222,7 @@ extern "C" int pidb_pair_sums(const void* u, const void* v, int dtype, int64_t m
                               int op, double* out_host, void* ws, size_t ws_bytes,
                               void* stream) {
   PIDB_REQUIRE(u && v && out_host && m >= 1, "bad arguments to pidb_pair_sums");
+  PIDB_REQUIRE(dtype == PIDB_F32 || dtype == PIDB_F64, "dtype must be PIDB_F32 or PIDB_F64");
   PIDB_REQUIRE(op >= PIDB_OP_INCLUSION && op <= PIDB_OP_MINMAX, "unknown pair op %d", op);
   const int nb = (int)std::min<int64_t>(4 * 148, (m + 255) / 256);
   PIDB_REQUIRE(ws && ws_bytes >= (size_t)(4 * nb + 4) * sizeof(double),
@@ -281,6 +289,7 @@ __global__ void mean_mask_kernel(const T* __restrict__ u, int64_t n, int64_t m, 
 extern "C" int pidb_mean_mask(const void* u, int dtype, int64_t n, int64_t m, int64_t ld,
                               double* out, void* stream) {
   PIDB_REQUIRE(u && out && n >= 1 && m >= 1 && ld >= m, "bad arguments to pidb_mean_mask");
+  PIDB_REQUIRE(dtype == PIDB_F32 || dtype == PIDB_F64, "dtype must be PIDB_F32 or PIDB_F64");
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 148 * 8));
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == PIDB_F32)
@@ -429,6 +438,7 @@ extern "C" int pidb_sum_rows(const double* src, int64_t rows, int64_t len, doubl
 extern "C" int pidb_validate(void* u, int dtype, int64_t n, int64_t m, int64_t ld, int clamp,
                              void* stats, void* stream) {
   PIDB_REQUIRE(u && stats && n >= 1 && m >= 1 && ld >= m, "bad arguments to pidb_validate");
+  PIDB_REQUIRE(dtype == PIDB_F32 || dtype == PIDB_F64, "dtype must be PIDB_F32 or PIDB_F64");
   cudaStream_t st = (cudaStream_t)stream;
   unsigned long long* nf = static_cast<unsigned long long*>(stats);
   long long* kmin = reinterpret_cast<long long*>(nf + 1);

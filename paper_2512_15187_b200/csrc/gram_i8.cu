@@ -8,9 +8,16 @@
 //
 // Kernel: C = A B^T tiles of 128 x 256 with A = members [128 ib, +128),
 // B = members [256 jb, +256) (upper tile triangle only, the Gram is
-// symmetric), K = cells split across CTAs.  The packed members are 16 KB
-// tiles (128 members x 128 cells, already in the 128-byte-swizzled K-major
-// order), so a stage is three plain 1D bulk copies.  Warp roles (192 threads):
+// symmetric), K = cells split across CTAs.  Operands come from one of two
+// layouts:
+//   * the K7 tiles of fp32/fp64 members: 16 KB tiles (128 members x 128
+//     cells, already in the 128-byte-swizzled K-major order), a stage is
+//     three plain 1D bulk copies;
+//   * a byte ensemble (0/1 members stored as uint8, row pitch ld): the same
+//     three 128 x 128-byte boxes by 2D TMA with SWIZZLE_128B straight from
+//     the member matrix -- no pack pass; rows >= n and cells >= m are the
+//     TMA's zero fill.
+// Warp roles (192 threads):
 //   warp 0 : bulk-copy producer (4-stage ring)
 //   warp 1 : single-thread tcgen05.mma.kind::i8 issuer (M=128, N=256, K=32),
 //            int32 accumulators in TMEM (exact: < 2^31 cells per pair)
@@ -44,8 +51,10 @@ __device__ __forceinline__ void tile_of(int t, int nib, int& ib, int& jb) {
   ib = t;
 }
 
+template <bool kBytes>
 __global__ void __launch_bounds__(kGramThreads, 1)
-    gram_i8_kernel(const uint8_t* __restrict__ tiles, const GramI8Params p) {
+    gram_i8_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ tiles,
+                   const GramI8Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   unsigned char* ring = smem_raw + pad;
@@ -72,6 +81,7 @@ __global__ void __launch_bounds__(kGramThreads, 1)
     fence_mbar_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, kBN);
+  if (kBytes && warp == 0 && lane == 0) prefetch_tma_desc(&tmap);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -86,15 +96,22 @@ __global__ void __launch_bounds__(kGramThreads, 1)
         mbar_wait(&empty[s], ph ^ 1u);
         unsigned char* a = ring + s * kStageBytes;
         mbar_arrive_expect_tx(&full[s], kStageBytes);
-        const int64_t kb = kb0 + k;  // three contiguous 16 KB tiles: A, then B's two halves
+        const int64_t kb = kb0 + k;  // three 16 KB tiles: A, then B's two halves
         PIDB_DCHECK(kb < p.kblocks && ib < 2 * ((p.n + 255) / 256) &&
                         2 * jb + 1 < 2 * ((p.n + 255) / 256),
                     "K2 operand tile bounds");
-        bulk_load(a, tiles + ((int64_t)ib * p.kblocks + kb) * kABytes, kABytes, &full[s], pol);
-        bulk_load(a + kABytes, tiles + ((int64_t)(2 * jb) * p.kblocks + kb) * kABytes, kABytes,
-                  &full[s], pol);
-        bulk_load(a + 2 * kABytes, tiles + ((int64_t)(2 * jb + 1) * p.kblocks + kb) * kABytes,
-                  kABytes, &full[s], pol);
+        if constexpr (kBytes) {
+          const int32_t x = (int32_t)(kb * kBK);
+          tma_load_2d(a, &tmap, x, ib * kBM, &full[s], pol);
+          tma_load_2d(a + kABytes, &tmap, x, 2 * jb * kBM, &full[s], pol);
+          tma_load_2d(a + 2 * kABytes, &tmap, x, (2 * jb + 1) * kBM, &full[s], pol);
+        } else {
+          bulk_load(a, tiles + ((int64_t)ib * p.kblocks + kb) * kABytes, kABytes, &full[s], pol);
+          bulk_load(a + kABytes, tiles + ((int64_t)(2 * jb) * p.kblocks + kb) * kABytes, kABytes,
+                    &full[s], pol);
+          bulk_load(a + 2 * kABytes, tiles + ((int64_t)(2 * jb + 1) * p.kblocks + kb) * kABytes,
+                    kABytes, &full[s], pol);
+        }
         if (++s == kStages) { s = 0; ph ^= 1u; }
       }
     }
@@ -208,24 +225,43 @@ extern "C" size_t pidb_gram_i8_workspace_bytes(int64_t n, int64_t m) {
   return plan_i8(n, m).ws;
 }
 
-extern "C" int pidb_gram_i8(const uint8_t* tiles, int64_t n, int64_t m, int64_t* gram, void* ws,
-                            size_t ws_bytes, void* stream) {
-  PIDB_REQUIRE(tiles && gram && n >= 1 && m >= 1, "bad arguments to pidb_gram_i8");
-  PIDB_REQUIRE((reinterpret_cast<uintptr_t>(tiles) & 1023) == 0, "tiles must be 1 KB aligned");
-  PIDB_REQUIRE(m < ((int64_t)1 << 31), "int32 tensor-core accumulators need m < 2^31 cells");
-  PIDB_REQUIRE(n <= (1 << 20), "too many members for the integer Gram");
+static int launch_i8(const CUtensorMap& tmap, const uint8_t* tiles, bool bytes, int64_t n,
+                     int64_t m, int64_t* gram, void* ws, size_t ws_bytes, cudaStream_t st) {
   const GramPlan g = plan_i8(n, m);
   PIDB_REQUIRE(ws && ws_bytes >= g.ws, "workspace too small: need %zu bytes", g.ws);
   GramI8Params p{};
   p.n = (int)n; p.nib = g.nib; p.njb = g.njb; p.ntiles = g.ntiles; p.splits = g.splits;
   p.kblocks = g.kblocks; p.kb_per = g.kb_per;
   p.part = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + 256);
-  cudaStream_t st = (cudaStream_t)stream;
-  PIDB_CUDA(cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)g.smem));
-  gram_i8_kernel<<<g.units, kGramThreads, g.smem, st>>>(tiles, p);
+  auto kern = bytes ? gram_i8_kernel<true> : gram_i8_kernel<false>;
+  PIDB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+  kern<<<g.units, kGramThreads, g.smem, st>>>(tmap, tiles, p);
   PIDB_LAUNCH_CHECK("gram_i8_kernel");
   gram_i8_reduce_kernel<<<g.ntiles * 32, 256, 0, st>>>(p.part, (int)n, g.nib, g.splits, gram);
   PIDB_LAUNCH_CHECK("gram_i8_reduce_kernel");
   return PIDB_OK;
+}
+
+extern "C" int pidb_gram_i8(const uint8_t* tiles, int64_t n, int64_t m, int64_t* gram, void* ws,
+                            size_t ws_bytes, void* stream) {
+  PIDB_REQUIRE(tiles && gram && n >= 1 && m >= 1, "bad arguments to pidb_gram_i8");
+  PIDB_REQUIRE((reinterpret_cast<uintptr_t>(tiles) & 1023) == 0, "tiles must be 1 KB aligned");
+  PIDB_REQUIRE(m < ((int64_t)1 << 31), "int32 tensor-core accumulators need m < 2^31 cells");
+  PIDB_REQUIRE(n <= (1 << 20), "too many members for the integer Gram");
+  CUtensorMap unused{};
+  return launch_i8(unused, tiles, false, n, m, gram, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int pidb_gram_i8_bytes(const uint8_t* u, int64_t n, int64_t m, int64_t ld,
+                                  int64_t* gram, void* ws, size_t ws_bytes, void* stream) {
+  PIDB_REQUIRE(u && gram && n >= 1 && m >= 1 && ld >= m, "bad arguments to pidb_gram_i8_bytes");
+  PIDB_REQUIRE((reinterpret_cast<uintptr_t>(u) & 15) == 0 && ld % 16 == 0,
+               "byte members need a 16-byte aligned base and row pitch");
+  PIDB_REQUIRE(m < ((int64_t)1 << 31), "int32 tensor-core accumulators need m < 2^31 cells");
+  PIDB_REQUIRE(n <= (1 << 20), "too many members for the integer Gram");
+  CUtensorMap tmap;
+  const int rc = encode_tma_2d(&tmap, u, CU_TENSOR_MAP_DATA_TYPE_UINT8, (uint64_t)m, (uint64_t)n,
+                               (uint64_t)ld, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc != PIDB_OK) return rc;
+  return launch_i8(tmap, nullptr, true, n, m, gram, ws, ws_bytes, (cudaStream_t)stream);
 }

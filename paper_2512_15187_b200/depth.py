@@ -302,7 +302,7 @@ def _finish(de, out: _Out, method: str, masses: np.ndarray, t0: float) -> DepthR
 def member_masses(ensemble, workers: int | None = None, require_binary: bool = False) -> np.ndarray:
     """Weighted mass of every member (depth.py:88-102), one device pass."""
     resolve_workers(workers)
-    de = stage(ensemble)
+    de = stage(ensemble).prob()
     if require_binary:
         mass, nb = _masses_device(de, with_nonbinary=True)
         _raise_first_nonbinary(de, nb)
@@ -340,7 +340,7 @@ def depth_pid_mean(ensemble, workers: int | None = None,
     resolve_workers(workers)
     if _streamable(ensemble):
         return _pid_mean_streamed(ensemble, t0, cv_warn_threshold)
-    de = stage(ensemble)
+    de = stage(ensemble).prob()
     n, dev = de.n, de.device
 
     def enqueue():
@@ -619,7 +619,7 @@ def depth_pid(ensemble, workers: int | None = None, *, algorithm: str = "auto") 
     resolve_workers(workers)
     if algorithm not in PID_ALGORITHMS:
         raise ValidationError(f"unknown pid algorithm {algorithm!r}; expected one of {PID_ALGORITHMS}")
-    de = stage(ensemble)
+    de = stage(ensemble).prob()
     n = de.n
     if algorithm == "gram":
         out = _Out(n, de.device)
@@ -639,12 +639,15 @@ def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
     """Inclusion depth of binary ensembles (depth.py:192-210).
 
     Unit weights: exact integer intersection Gram (K7 pack + K2 tcgen05
-    kind::i8) and an exactly rounded epilogue, bit-identical to the
-    exact-summation oracle ref_eid.  Weighted grids: factorised Gram sums.
+    kind::i8; a byte ensemble goes to K2 directly) and an exactly rounded
+    epilogue, bit-identical to the exact-summation oracle ref_eid.
+    Weighted grids: factorised Gram sums.
     """
     t0 = time.perf_counter()
     resolve_workers(workers)
     de = stage(ensemble)
+    if de.weights is not None:
+        de = de.prob()
     n, dev = de.n, de.device
     if de.weights is None:
         from .reduction import intersection_gram, pack_binary
@@ -652,13 +655,17 @@ def depth_eid(ensemble, workers: int | None = None) -> DepthResult:
         def enqueue():
             # K7 packs and counts non-binary values in the same pass (the
             # counts ride in the result block); the masses are the Gram
-            # diagonal |C_i| (exact integers)
+            # diagonal |C_i| (exact integers).  Byte ensembles were checked
+            # when staged and need no pack.
             out = _Out(n, dev, extra=n)
             nb = out.extra.view(torch.int64)
             nb.zero_()
-            packed = pack_binary(de, nb)
-            _allreduce(nb, de)
-            g = intersection_gram(de, packed)
+            if de.is_bits:
+                g = intersection_gram(de)
+            else:
+                packed = pack_binary(de, nb)
+                _allreduce(nb, de)
+                g = intersection_gram(de, packed)
             mslot, ii, io, d = out.ptrs()
             N.call("pidb_eid_exact_epilogue", g.data_ptr(), n, ii, io, d, out.rank.data_ptr(),
                    mslot, stream_ptr(dev))
@@ -702,7 +709,7 @@ def depth_similarity_baseline(ensemble, measure: str, workers: int | None = None
         ) from None
     t0 = time.perf_counter()
     resolve_workers(workers)
-    de = stage(ensemble)
+    de = stage(ensemble).prob()
     n, dev = de.n, de.device
 
     def enqueue():
@@ -730,7 +737,7 @@ def compare_pid_vs_mean(ensemble, workers: int | None = None) -> dict:
     """Exact PID vs PID-mean: depth error and rank agreement (depth.py:328-346)."""
     from .consistency import kendall_tau, pearson
 
-    de = stage(ensemble)
+    de = stage(ensemble).prob()
     if de.n < 2:
         raise ValidationError("comparison needs at least two members")
     exact = depth_pid(de, workers)

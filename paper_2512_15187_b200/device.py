@@ -8,7 +8,10 @@ depth kernel then streams the resident matrix.
 Layout: row i = member i, ``ld`` = cells rounded up to 32 elements (128-byte
 rows, TMA-aligned), zero padding.  float32 storage unless a member is float64
 (the reference's dtype policy, grid.py:103-104), in which case the whole matrix
-is float64.  A sharded ensemble holds a contiguous cell slab [lo, hi) of every
+is float64.  A bool / uint8 tensor is staged as a byte ensemble (0/1 members,
+one byte per cell, checked once here like BinaryMask, grid.py:145-148): eID
+reads it directly (no pack pass, a quarter of the fp32 bytes); every other
+method sees its cached float32 view (``prob()``, binarize(...).to_prob()).  A sharded ensemble holds a contiguous cell slab [lo, hi) of every
 member on each rank (multi-GPU voxel sharding).
 """
 from __future__ import annotations
@@ -52,7 +55,7 @@ def shard_bounds(m: int, rank: int, world: int) -> tuple[int, int]:
 
 @dataclass
 class DeviceEnsemble:
-    values: torch.Tensor                 # (n, ld) float32/float64 on a CUDA device
+    values: torch.Tensor                 # (n, ld) float32/float64 (or 0/1 uint8) on a CUDA device
     m: int                               # cells held here (shard-local)
     dims: tuple[int, ...]
     ids: tuple[str, ...]
@@ -77,7 +80,28 @@ class DeviceEnsemble:
 
     @property
     def dtype_code(self) -> int:
+        if self.values.dtype == torch.uint8:
+            return N.PIDB_U8
         return N.PIDB_F64 if self.values.dtype == torch.float64 else N.PIDB_F32
+
+    @property
+    def is_bits(self) -> bool:
+        """0/1 members stored one byte per cell (a binary ensemble)."""
+        return self.values.dtype == torch.uint8
+
+    def prob(self) -> "DeviceEnsemble":
+        """The float32 ensemble of a byte ensemble (binarize(...).to_prob(),
+        grid.py:152-153, 271-277), widened on the device once and cached;
+        ``self`` for a float ensemble."""
+        if not self.is_bits:
+            return self
+        p = self._cache.get("prob")
+        if p is None:
+            p = DeviceEnsemble(self.values.to(torch.float32), self.m, self.dims, self.ids,
+                               self.weights, self.weights_host, self.process_group,
+                               self.cell_range)
+            self._cache["prob"] = p
+        return p
 
     @property
     def grid(self) -> GridSpec:
@@ -132,6 +156,13 @@ class DeviceEnsemble:
         ids = _make_ids(ids, n)
         w_host, w_dev = _weights(weights, m, dev)
         flat = values.reshape(n, m)
+        if flat.dtype in (torch.bool, torch.uint8):  # byte ensemble
+            src = flat if flat.dtype == torch.uint8 else flat.view(torch.uint8)
+            de = cls(_copy_padded(src, torch.uint8, dev), m, dims, ids, w_dev, w_host,
+                     process_group, cr)
+            if validate and flat.dtype == torch.uint8:
+                _check_bits(de)
+            return de
         es = 8 if dt == torch.float64 else 4
         if (flat.is_cuda and flat.device == dev and flat.dtype == dt and flat.stride(1) == 1
                 and (flat.stride(0) * es) % 16 == 0 and flat.data_ptr() % 16 == 0):
@@ -165,13 +196,13 @@ class DeviceEnsemble:
 
         if self.sharded:
             raise ValidationError("a sharded ensemble holds only this rank's cells")
-        return ProbMask(self.grid, self.values[i, :self.m].cpu().numpy())
+        return ProbMask(self.grid, self.prob().values[i, :self.m].cpu().numpy())
 
     def __iter__(self):
         return (self.member(i) for i in range(self.n))
 
     def block_values(self, lo: int, hi: int) -> np.ndarray:
-        return self.values[lo:hi, :self.m].cpu().numpy()
+        return self.prob().values[lo:hi, :self.m].cpu().numpy()
 
     def subset(self, indices: Sequence[int]) -> "DeviceEnsemble":
         """Members ``indices`` in the given order (grid.py Ensemble.subset);
@@ -204,9 +235,10 @@ class DeviceEnsemble:
         return ws
 
     def mean_values(self) -> torch.Tensor:
-        out = torch.empty(self.m, dtype=torch.float64, device=self.device)
-        N.call("pidb_mean_mask", self.ptr(), self.dtype_code, self.n, self.m, self.ld,
-               out.data_ptr(), stream_ptr(self.device))
+        de = self.prob()
+        out = torch.empty(de.m, dtype=torch.float64, device=de.device)
+        N.call("pidb_mean_mask", de.ptr(), de.dtype_code, de.n, de.m, de.ld,
+               out.data_ptr(), stream_ptr(de.device))
         return out
 
 
@@ -257,6 +289,16 @@ def _copy_padded(flat: torch.Tensor, dt, dev) -> torch.Tensor:
     if not src.is_cuda and not src.is_pinned():
         torch.cuda.current_stream(dev).synchronize()  # pageable source must outlive the copy
     return out
+
+
+def _check_bits(de: "DeviceEnsemble") -> None:
+    """BinaryMask's value check (grid.py:145-148) on a byte ensemble: K7 in
+    count-only mode."""
+    bad = torch.zeros(de.n, dtype=torch.int64, device=de.device)
+    N.call("pidb_binary_pack", de.ptr(), N.PIDB_U8, de.n, de.m, de.ld, None, bad.data_ptr(),
+           stream_ptr(de.device))
+    if bool((bad.cpu() != 0).any()):
+        raise ValidationError("binary mask values must be 0 or 1")
 
 
 def _key_to_double(k: int) -> float:
@@ -312,6 +354,8 @@ def stage(ensemble, device=None, shard: tuple[int, int] | None = None,
     reference-style Ensemble (``grid``, ``ids``, ``len``, ``member(i)``;
     lazy loaders are resolved one member at a time, grid.py:196-202).
     ``shard=(rank, world)`` keeps only this rank's contiguous cell slab.
+    A bool / uint8 tensor becomes a byte ensemble; the methods other than
+    depth_eid read its float32 view (``stage(x).prob()``).
     """
     if isinstance(ensemble, DeviceEnsemble):
         return ensemble

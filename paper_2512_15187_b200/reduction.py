@@ -99,15 +99,20 @@ def pack_binary(de: DeviceEnsemble, nonbinary: torch.Tensor | None = None) -> to
 
 
 def intersection_gram(de: DeviceEnsemble, packed: torch.Tensor | None = None) -> torch.Tensor:
-    """I[i, j] = |C_i ∩ C_j| exactly (int64), via K7 + K2."""
+    """I[i, j] = |C_i ∩ C_j| exactly (int64), via K7 + K2 (K2 alone on a
+    byte ensemble, whose members it loads by TMA)."""
     lib = N.load()
-    b = pack_binary(de) if packed is None else packed
     g = torch.empty((de.n, de.n), dtype=torch.int64, device=de.device)
     ws = de.workspace(lib.pidb_gram_i8_workspace_bytes(de.n, de.m))
     from .depth import _launch
 
-    _launch("pidb_gram_i8", b.data_ptr(), de.n, de.m, g.data_ptr(), ws.data_ptr(), ws.numel(),
-            stream_ptr(de.device))
+    if de.is_bits and packed is None:
+        _launch("pidb_gram_i8_bytes", de.ptr(), de.n, de.m, de.ld, g.data_ptr(), ws.data_ptr(),
+                ws.numel(), stream_ptr(de.device))
+    else:
+        b = pack_binary(de) if packed is None else packed
+        _launch("pidb_gram_i8", b.data_ptr(), de.n, de.m, g.data_ptr(), ws.data_ptr(),
+                ws.numel(), stream_ptr(de.device))
     _allreduce(g, de)
     return g
 

@@ -541,6 +541,78 @@ def test_cell_permutation_invariance(pb):
     np.testing.assert_array_equal(base.rank, shuf.rank)
 
 
+@pytest.mark.parametrize("n,m,density", [(1, 1, 1.0), (3, 4, 0.5), (8, 25, 0.5), (130, 1000, 0.3),
+                                         (257, 4097, 0.6), (500, 20000, 0.42), (700, 333, 0.9),
+                                         (129, 128, 0.5), (255, 129, 0.2), (1000, 16, 0.7)])
+def test_byte_ensemble_gram_and_eid(pb, n, m, density):
+    """A bool / uint8 ensemble is held as bytes and K2 loads it by TMA (no
+    pack): its intersection Gram equals the exact integer counts, and its eID
+    is bit-identical to the fp32 ensemble's and to the exact oracle."""
+    from paper_2512_15187_b200.reduction import intersection_gram
+
+    rng = np.random.default_rng(n * 11 + m)
+    B = rng.uniform(size=(n, m)) < density
+    de_b = pb.stage(torch.from_numpy(B))
+    de_u = pb.stage(torch.from_numpy(B.astype(np.uint8)))
+    assert de_b.is_bits and de_u.is_bits
+    want_g = exact.intersections(B.astype(np.float32))
+    np.testing.assert_array_equal(intersection_gram(de_b).cpu().numpy(), want_g)
+    np.testing.assert_array_equal(intersection_gram(de_u).cpu().numpy(), want_g)
+    rf = pb.depth_eid(torch.from_numpy(B.astype(np.float32)))
+    for de in (de_b, de_u, B):
+        r = pb.depth_eid(de)
+        for k in ("in_in", "in_out", "depth"):
+            assert np.array_equal(getattr(r, k), getattr(rf, k)), k
+        np.testing.assert_array_equal(r.rank, rf.rank)
+    a, b, c, _ = exact.eid_fast(B.astype(np.float32))
+    assert np.array_equal(rf.depth, c)
+
+
+def test_byte_ensemble_graph_replay_and_pitch(pb):
+    """Repeated eID calls on one staged byte ensemble replay a graph; a
+    caller-strided device matrix (pitch > cells) gives the same result."""
+    rng = np.random.default_rng(5)
+    B = rng.uniform(size=(300, 5000)) < 0.4
+    de = pb.stage(torch.from_numpy(B))
+    first = pb.depth_eid(de)
+    for _ in range(3):
+        again = pb.depth_eid(de)
+        assert np.array_equal(again.depth, first.depth)
+    wide = torch.zeros((300, 5120), dtype=torch.bool, device="cuda")
+    wide[:, :5000] = torch.from_numpy(B).cuda()
+    r = pb.depth_eid(wide[:, :5000])
+    assert np.array_equal(r.depth, first.depth)
+
+
+def test_byte_ensemble_rejects_non_binary(pb):
+    """uint8 members must be 0/1, as BinaryMask requires (grid.py:145-148)."""
+    U = np.zeros((4, 37), dtype=np.uint8)
+    U[2, 30] = 255
+    with pytest.raises(pb.ValidationError, match="binary mask values must be 0 or 1"):
+        pb.stage(torch.from_numpy(U))
+    U[2, 30] = 2
+    with pytest.raises(pb.ValidationError, match="binary mask values must be 0 or 1"):
+        pb.depth_eid(U)
+
+
+def test_byte_ensemble_float_methods(pb):
+    """Every other method reads the byte ensemble's float32 view and returns
+    exactly what the float32 ensemble gives; weighted eID too."""
+    rng = np.random.default_rng(9)
+    B = rng.uniform(size=(40, 3000)) < 0.5
+    F = torch.from_numpy(B.astype(np.float32))
+    de = pb.stage(torch.from_numpy(B))
+    for fn in (pb.depth_pid, pb.depth_pid_mean, lambda e: pb.depth_similarity_baseline(e, "dice")):
+        a, b = fn(de), fn(F)
+        assert np.array_equal(a.depth, b.depth)
+    assert np.array_equal(pb.member_masses(de), pb.member_masses(F))
+    assert np.array_equal(de.member(3).values, B[3].astype(np.float32))
+    w = rng.uniform(0.5, 2.0, size=3000)
+    dw = pb.DeviceEnsemble.from_tensor(torch.from_numpy(B), w)
+    fw = pb.DeviceEnsemble.from_tensor(F, w)
+    assert np.array_equal(pb.depth_eid(dw).depth, pb.depth_eid(fw).depth)
+
+
 def test_eid_equals_pid_on_binary(pb):
     for seed in range(6):
         U, _ = make_binary(seed, 6, (4, 4))

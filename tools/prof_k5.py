@@ -1,6 +1,7 @@
 """Small driver for timing / ncu captures of the streaming kernels:
-python tools/prof_k5.py N RES [pid-mean|pid|pid:gram|dice|mass|eid] [reps]
-(eid: N binary Fourier contours on a RES^2 grid)
+python tools/prof_k5.py N RES [pid-mean|pid|pid:gram|dice|mass|eid|eid:bits] [reps]
+(eid: N binary Fourier contours on a RES^2 grid, as fp32; eid:bits the same
+contours as a byte ensemble)
 Prints the per-call time and the per-kernel device times (CUDA events around
 each native launch, depth.KERNEL_EVENTS)."""
 import sys
@@ -17,8 +18,11 @@ from paper_2512_15187_b200 import synth  # noqa: E402
 n, res = int(sys.argv[1]), int(sys.argv[2])
 method = sys.argv[3] if len(sys.argv) > 3 else "pid-mean"
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
-de = synth.contours_device(n, res, 0) if method == "eid" else synth.ellipsoids_device(res, n, 0, 0)
-if method == "eid":
+eid = method.startswith("eid")
+de = synth.contours_device(n, res, 0) if eid else synth.ellipsoids_device(res, n, 0, 0)
+if method == "eid:bits":
+    de = pb.stage(de.values[:, :de.m] != 0)
+if eid:
     fn = pb.depth_eid
 elif method == "pid-mean":
     fn = pb.depth_pid_mean
@@ -47,6 +51,6 @@ per = defaultdict(float)
 for name, a, b in D.KERNEL_EVENTS:
     per[name] += a.elapsed_time(b) / reps
 D.KERNEL_EVENTS = None
-gb = n * (res**2 if method == "eid" else res**3) * 4 / 1e9
+gb = n * (res**2 if eid else res**3) * (1 if method == "eid:bits" else 4) / 1e9
 kern = " ".join(f"{k}={v:.3f}ms({gb / v:.0f}TB/s)" for k, v in per.items())
 print(f"n={n} res={res} {method}: {ms:.3f} ms/call | {kern}")
