@@ -291,13 +291,18 @@ def _copy_padded(flat: torch.Tensor, dt, dev) -> torch.Tensor:
     return out
 
 
-def _check_bits(de: "DeviceEnsemble") -> None:
-    """BinaryMask's value check (grid.py:145-148) on a byte ensemble: K7 in
-    count-only mode."""
+def _nonbinary_counts(de: "DeviceEnsemble") -> np.ndarray:
+    """Per-member count of bytes other than 0/1 in a byte ensemble (K7 in
+    count-only mode)."""
     bad = torch.zeros(de.n, dtype=torch.int64, device=de.device)
     N.call("pidb_binary_pack", de.ptr(), N.PIDB_U8, de.n, de.m, de.ld, None, bad.data_ptr(),
            stream_ptr(de.device))
-    if bool((bad.cpu() != 0).any()):
+    return bad.cpu().numpy()
+
+
+def _check_bits(de: "DeviceEnsemble") -> None:
+    """BinaryMask's value check (grid.py:145-148) on a byte ensemble."""
+    if _nonbinary_counts(de).any():
         raise ValidationError("binary mask values must be 0 or 1")
 
 

@@ -90,6 +90,31 @@ def test_stage_manifest_binary_threshold(pb, tmp_path):
         pb.stage_manifest(tmp_path / "bad.json")
 
 
+def test_stage_manifest_binary_is_byte_ensemble(pb, tmp_path):
+    """A manifest of uint8 / bool masks stages as a byte ensemble: eID reads
+    the bytes, the other methods its float32 view; results equal those of the
+    reference-loaded (float32) ensemble; a 0/2 member raises with its id."""
+    rng = np.random.default_rng(6)
+    (tmp_path / "v").mkdir()
+    entries = []
+    for i in range(5):
+        b = rng.uniform(size=(9, 11)) < rng.uniform(0.2, 0.8)
+        pb.write_volume(b if i % 2 else b.astype(np.uint8), tmp_path / f"v/b{i}.npy")
+        entries.append({"id": f"b{i}", "path": f"v/b{i}.npy"})
+    pb.write_manifest(tmp_path / "m.json", (9, 11), entries)
+    de = pb.stage_manifest(tmp_path / "m.json")
+    assert de.is_bits
+    e = pb.read_manifest(tmp_path / "m.json")
+    for fn in (pb.depth_eid, pb.depth_pid, pb.depth_pid_mean):
+        a, b = fn(de), fn(e)
+        assert np.array_equal(a.depth, b.depth) and np.array_equal(a.rank, b.rank)
+    bad = (rng.uniform(size=(9, 11)) < 0.5).astype(np.uint8) * 2
+    pb.write_volume(bad, tmp_path / "v/bad.npy")
+    pb.write_manifest(tmp_path / "bad.json", (9, 11), entries + [{"id": "two", "path": "v/bad.npy"}])
+    with pytest.raises(pb.ValidationError, match="'two': binary mask values must be 0 or 1"):
+        pb.stage_manifest(tmp_path / "bad.json")
+
+
 def test_stage_manifest_rejects_non_binary_uint8(pb, tmp_path):
     """A 0/255 uint8 mask loads through BinaryMask in the reference, which
     raises ValidationError (grid.py:145-147); staging it must raise too (and
