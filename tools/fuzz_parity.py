@@ -4,8 +4,8 @@ oracle: python tools/fuzz_parity.py SECONDS [seed]
 PID-mean / PID / dice / IoU / masses, binary eID, and -- round 2 -- the
 tensor-core PID (K1x + certifier: depths within 1e-8, ranks equal), the
 fp64 gram_block seam (rtol 1e-12) and, for pinned host inputs, the streamed
-PID-mean; depths within 1e-11, ranks equal wherever the oracle's depth gaps
-exceed 1e-11)."""
+PID-mean, and binary eID on byte ensembles; depths within 1e-11, ranks
+equal wherever the oracle's depth gaps exceed 1e-11)."""
 import sys
 import time
 import warnings
@@ -93,6 +93,11 @@ while time.time() < t_end:
             r = pb.depth_eid(de)
             if not (np.array_equal(r.depth, c) and np.array_equal(r.rank, exact.ranks(c))):
                 print(f"FAIL eid n={n} m={m}", flush=True)
+                fails += 1
+            # the same members as a byte ensemble (K2 straight from the bytes)
+            rb = pb.depth_eid(U != 0 if rng.uniform() < 0.5 else (U != 0).astype(np.uint8))
+            if not (np.array_equal(rb.depth, c) and np.array_equal(rb.rank, r.rank)):
+                print(f"FAIL eid-bytes n={n} m={m}", flush=True)
                 fails += 1
         for name, r, ref in checks:
             err = float(np.max(np.abs(r.depth - ref["depth"]))) if n else 0.0
