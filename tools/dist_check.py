@@ -43,15 +43,21 @@ for kind, n, dims, weighted in cases:
     methods = ["pid-mean", "pid", "dice", "iou"] + (["eid"] if kind == "binary" else [])
     got = {mth: pb.depth_by_method(de, mth) for mth in methods}
     got["pid-gram"] = pb.depth_pid(de, algorithm="gram")  # K1x per shard + allreduce
+    if kind == "binary":  # the slab as a byte ensemble: K2 from the bytes + allreduce
+        db = pb.DeviceEnsemble.from_tensor(torch.from_numpy(U[:, lo:hi] != 0), dims=dims,
+                                           process_group=pg, cell_range=(lo, hi))
+        got["eid-bytes"] = pb.depth_eid(db)
+        got["pid-bytes"] = pb.depth_pid(db)
     if rank == 0:
         full = pb.DeviceEnsemble.from_tensor(torch.from_numpy(U), w, dims=dims)
-        for mth in methods + ["pid-gram"]:
-            want = pb.depth_by_method(full, "pid" if mth == "pid-gram" else mth)
+        for mth in methods + [k for k in ("pid-gram", "eid-bytes", "pid-bytes") if k in got]:
+            want = pb.depth_by_method(full, {"pid-gram": "pid", "eid-bytes": "eid",
+                                             "pid-bytes": "pid"}.get(mth, mth))
             err = float(np.abs(got[mth].depth - want.depth).max())
             same = bool(np.array_equal(got[mth].rank, want.rank))
             exact = bool(np.array_equal(got[mth].depth, want.depth))
             tol = 1e-8 if mth == "pid-gram" else 1e-12  # tensor-core Gram bound vs exact
-            good = (exact if mth == "eid" else err <= tol) and same
+            good = (exact if mth in ("eid", "eid-bytes") else err <= tol) and same
             ok &= good
             print(f"{kind} n={n} m={m} w={weighted} {mth}: max|d| diff {err:.2e} "
                   f"ranks {'equal' if same else 'DIFFER'}{' bit-exact' if exact else ''}"
