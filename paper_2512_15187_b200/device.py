@@ -91,7 +91,9 @@ class DeviceEnsemble:
 
     def prob(self) -> "DeviceEnsemble":
         """The float32 ensemble of a byte ensemble (binarize(...).to_prob(),
-        grid.py:152-153, 271-277), widened on the device once and cached;
+        grid.py:152-153, 271-277), widened on the device once and cached
+        (4 bytes per cell next to the 1-byte matrix; in-place edits of the
+        bytes after the first call are not seen by it: restage instead);
         ``self`` for a float ensemble."""
         if not self.is_bits:
             return self
@@ -196,13 +198,18 @@ class DeviceEnsemble:
 
         if self.sharded:
             raise ValidationError("a sharded ensemble holds only this rank's cells")
-        return ProbMask(self.grid, self.prob().values[i, :self.m].cpu().numpy())
+        return ProbMask(self.grid, self._host_rows(i, i + 1)[0])
 
     def __iter__(self):
         return (self.member(i) for i in range(self.n))
 
     def block_values(self, lo: int, hi: int) -> np.ndarray:
-        return self.prob().values[lo:hi, :self.m].cpu().numpy()
+        return self._host_rows(lo, hi)
+
+    def _host_rows(self, lo: int, hi: int) -> np.ndarray:
+        rows = self.values[lo:hi, :self.m]
+        # a byte ensemble widens just these rows (not the cached full view)
+        return (rows.to(torch.float32) if self.is_bits else rows).cpu().numpy()
 
     def subset(self, indices: Sequence[int]) -> "DeviceEnsemble":
         """Members ``indices`` in the given order (grid.py Ensemble.subset);
