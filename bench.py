@@ -486,9 +486,15 @@ def run_ours(args, rank, world, local, pg):
         }
 
     # ---------------- parity at full size against the CPU reference
-    if rank == 0 and world == 1 and not args.no_parity and args.workload == "cfg5":
-        line["parity"] = {"cfg5_pid_mean_full": _guarded("cfg5 parity", parity_pid_mean_full, de,
-                                                         res_chk)}
+    if rank == 0 and world == 1 and not args.no_parity and method == "pid-mean":
+        line["parity"] = {f"{args.workload}_pid_mean_full": _guarded(
+            f"{args.workload} parity", parity_pid_mean_full, de, res_chk)}
+    elif rank == 0 and world == 1 and not args.no_parity and args.workload == "cfg4":
+        line["parity"] = {"cfg4_1000x64": _guarded("cfg4 1000x64^3 parity", parity_pid_reduced,
+                                                   dev)}
+    if "parity" in line and args.workload == "cfg1":  # cfg1 names full PID too (CPU-sized)
+        line["parity"]["cfg1_pid_full"] = _guarded("cfg1 pid parity", parity_pid_full, de,
+                                                   pb.depth_pid(de))
 
     # ---------------- end to end from pinned host memory
     host = None
@@ -550,6 +556,22 @@ def parity_pid_mean_full(de, got):
     ref = fd.depth_pid_mean(reference.lazy_from_device(fd, de), workers=workers)
     out = {"reference": cpu_what(), "size": f"{de.n} x {de.m} cells (full config, "
                                              f"{de.n * de.m:.3e} member-voxels)",
+           "reference_seconds": time.perf_counter() - t0, "workers": workers}
+    out.update(_agreement(got, ref))
+    return out
+
+
+def parity_pid_full(de, got):
+    """Full-size depth_pid of the REAL reference on the same device bytes."""
+    fd = reference_module()
+    if fd is None:
+        return {"skipped": "baseline/_ref not installed (tools/install_reference.sh)"}
+    from oracle import reference
+
+    workers = min(16, os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    ref = fd.depth_pid(reference.lazy_from_device(fd, de), workers=workers)
+    out = {"reference": cpu_what(), "size": f"{de.n} x {de.m} cells (full config)",
            "reference_seconds": time.perf_counter() - t0, "workers": workers}
     out.update(_agreement(got, ref))
     return out
