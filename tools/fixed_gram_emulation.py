@@ -46,7 +46,7 @@ for name, U in (("ellipsoids", np.stack([e.member(i).values for i in range(len(e
     X = U.astype(np.float64)
     G, m = X @ X.T, X.sum(1)
     d = depth_from_gram(G, m)
-    for lv in (3, 4):
+    for lv in (1, 2, 3, 4):
         df = depth_from_gram(gram_fx(U, lv), m)
         swaps = int((np.argsort(-df, kind="stable") != np.argsort(-d, kind="stable")).sum())
         print(f"{name}: levels <= {lv}: max depth err {np.abs(df - d).max():.2e}, "
