@@ -674,6 +674,7 @@ def run_e2e(args, host, _, meta, fn, world, pg, dev, resident=None):
         check = {"max_abs_depth_diff_vs_resident": float(np.abs(r.depth - resident.depth).max()),
                  "ranks_equal_resident": bool(np.array_equal(r.rank, resident.rank))}
     total = n * int(np.prod(dims))
+    probe = h2d_probe(host, dev)
     path = ("depth_pid_mean(pinned host tensor): cell slabs of "
             f"{D.STREAM_SLAB_BYTES >> 20} MB, H2D on a side stream overlapped with in-place "
             "validation + K5 on two HBM slab buffers, fixed-order slab sum, K4, result D2H"
@@ -684,7 +685,29 @@ def run_e2e(args, host, _, meta, fn, world, pg, dev, resident=None):
             "steps": E2E_STEPS, "warmup": 3,
             "h2d_bytes_per_step": n * m * 4, "d2h_bytes_per_step": (5 * n + n + 1) * 8,
             "h2d_GBps_effective": n * m * 4 / (ms * 1e-3) / 1e9,
+            "h2d_GBps_probe": probe,
+            "frac_of_h2d_probe": n * m * 4 / (ms * 1e-3) / 1e9 / probe if probe else None,
             "bound": "PCIe host-to-device copy", "path": path, "check": check}
+
+
+def h2d_probe(host, dev, nbytes=4 << 30):
+    """Plain pinned H2D bandwidth on this box (best of 3 copies of up to
+    4 GB of the e2e host buffer): the e2e roofline."""
+    import torch
+
+    flat = host.reshape(-1).view(torch.uint8)
+    k = min(nbytes, flat.numel())
+    dst = torch.empty(k, dtype=torch.uint8, device=dev)
+    best = 0.0
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(flat[:k], non_blocking=True)
+        b.record()
+        b.synchronize()
+        best = max(best, k / (a.elapsed_time(b) * 1e-3) / 1e9)
+    del dst
+    return best
 
 
 # cuBLAS TF32 / INT8 dense GEMM peaks measured on this pool's B200 by
