@@ -56,6 +56,7 @@ struct Plan {
   uint32_t stage_bytes;
   size_t smem;
   int64_t tiles;
+  int rb = kRowBytes;  // bytes of a member row per tile (512: wide rows, fp32 n <= ~210)
 };
 
 // warp-specialised kernels, one translation unit per element type;
@@ -93,12 +94,13 @@ struct Vec<double> {
 
 __device__ __forceinline__ bool is_nonbinary(double x) { return !(x == 0.0 || x == 1.0); }
 
-// Column sweep over 256-byte rows: this thread's 16-byte chunk of rows
-// r0, r0 + kPhases, ... < r_end, starting at `pa`.  fp32 MODE_MEAN uses the
+// Column sweep over RB-byte rows: this thread's 16-byte chunk of rows
+// r0, r0 + kPh, ... < r_end, starting at `pa`.  fp32 MODE_MEAN uses the
 // Fast2Sum state; otherwise part[] += iv(row) * u in fp64.
-template <typename T, int NT = kThreads>
+template <typename T, int NT = kThreads, int RB = kRowBytes>
 struct ColSweep {
-  static constexpr int kPh = NT / kChunks16;  // row phases
+  static constexpr int kCh = RB / 16;        // 16-byte chunks per row
+  static constexpr int kPh = NT / kCh;       // row phases
   static constexpr int EPC = Vec<T>::EPC;
   float2 sh01, sh23, sc01, sc23;
   double part[EPC];
@@ -114,7 +116,7 @@ struct ColSweep {
     if constexpr (sizeof(T) == 4) {
       if (mode == MODE_MEAN) {
 #pragma unroll 4
-        for (int r = r0; r < r_end; r += kPh, pa += kPh * kRowBytes) {
+        for (int r = r0; r < r_end; r += kPh, pa += kPh * RB) {
           const float4 v = Vec<float>::loadf(pa);
           fast2sum_acc2(sh01, sc01, make_float2(v.x, v.y));
           fast2sum_acc2(sh23, sc23, make_float2(v.z, v.w));
@@ -123,7 +125,7 @@ struct ColSweep {
       }
     }
 #pragma unroll 4
-    for (int r = r0; r < r_end; r += kPh, rg += kPh, pa += kPh * kRowBytes) {
+    for (int r = r0; r < r_end; r += kPh, rg += kPh, pa += kPh * RB) {
       double v[EPC];
       Vec<T>::load(pa, v);
       const double iv = mode == MODE_MEAN ? 1.0 : (rg < n ? __ldg(inv + rg) : 0.0);
@@ -131,8 +133,9 @@ struct ColSweep {
       for (int e = 0; e < EPC; ++e) part[e] = fma(iv, v[e], part[e]);
     }
   }
-  // fold the Fast2Sum state into part[] and combine the warp's two row
-  // phases (lanes l and l^16 share a chunk); lanes < 16 hold the result
+  // fold the Fast2Sum state into part[] and, for 256-byte rows, combine the
+  // warp's two row phases (lanes l and l^16 share a chunk; lanes < 16 hold
+  // the result); with 512-byte rows a warp is one phase, every lane a chunk
   __device__ void combine(int mode) {
     if constexpr (sizeof(T) == 4) {
       if (mode == MODE_MEAN) {
@@ -142,8 +145,10 @@ struct ColSweep {
         part[3] = ((double)sh23.y - 1.0) + (double)sc23.y;
       }
     }
+    if constexpr (kCh < 32) {
 #pragma unroll
-    for (int e = 0; e < EPC; ++e) part[e] += __shfl_xor_sync(0xffffffffu, part[e], 16);
+      for (int e = 0; e < EPC; ++e) part[e] += __shfl_xor_sync(0xffffffffu, part[e], 16);
+    }
   }
 };
 
@@ -301,16 +306,18 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <typename T, int ROWS, int MODE, bool CL>
+template <typename T, int ROWS, int MODE, bool CL, int RB = kRowBytes>
 __global__ void __launch_bounds__(kRowsThreads, 1)
     rows_ws_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
+  static_assert(RB == kRowBytes || (!CL && sizeof(T) == 4), "wide rows: fp32, single CTA");
   constexpr int kWsColWarps = ws_col_warps(MODE);
   constexpr int kWsColThreads = kWsColWarps * 32;
   constexpr int kWsRowWarps = kRowsWarps - kWsColWarps;
   constexpr int kWsRowThreads = kWsRowWarps * 32;
   constexpr int EPC = Vec<T>::EPC;
-  constexpr int V = kRowBytes / (int)sizeof(T);
-  constexpr int EPL = 8 / (int)sizeof(T);
+  constexpr int V = RB / (int)sizeof(T);
+  constexpr int EPL = RB / 32 / (int)sizeof(T);  // cells per lane per row (row group)
+  constexpr int kCh = RB / 16;
   constexpr int kAll = kWsColThreads + kWsRowThreads;
   constexpr int SWEEP = MODE == MODE_SIM ? MODE_MEAN : MODE;
 
@@ -359,7 +366,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   if constexpr (CL) cluster_sync();  // peers' mbarriers exist before any st.async
   auto issue = [&](int64_t j) {
     const int s = (int)(j % p.stages);
-    mbar_arrive_expect_tx(&full[s], (uint32_t)box * kRowBytes);
+    mbar_arrive_expect_tx(&full[s], (uint32_t)box * RB);
     tma_load_2d(tiles + (size_t)s * p.stage_bytes, &tmap, (int32_t)((cid + j * ncl) * V), r0,
                 &full[s], pol);
   };
@@ -373,9 +380,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 
   if (warp < kWsColWarps) {
     // ---------------------------------------------------------- column group
-    const int q = tid & (kChunks16 - 1), ph = tid / kChunks16;
-    const uint32_t p1_off = (uint32_t)(ph * kRowBytes + q * 16);
-    ColSweep<T, kWsColThreads> csw;
+    const int q = tid & (kCh - 1), ph = tid / kCh;
+    const uint32_t p1_off = (uint32_t)(ph * RB + q * 16);
+    ColSweep<T, kWsColThreads, RB> csw;
     int s = 0;
     uint32_t par = 0;
     for (int64_t j = 0; j < my_tiles; ++j) {
@@ -397,7 +404,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         csw.reset();
         csw.run(tiles + (size_t)s * p.stage_bytes + p1_off, ph, box, SWEEP, p.inv, r0 + ph, n);
         csw.combine(SWEEP);
-        if (lane < 16) {
+        if (kCh == 32 || lane < 16) {
 #pragma unroll
           for (int e = 0; e < EPC; ++e) red[warp * V + q * EPC + e] = csw.part[e];
         }
@@ -441,7 +448,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   } else {
     // ------------------------------------------------------------- row group
     const int rw = warp - kWsColWarps;
-    const uint32_t p2_off = (uint32_t)(rw * kRowBytes + lane * 8);
+    const uint32_t p2_off = (uint32_t)(rw * RB + lane * (RB / 32));
     const int cell = lane * EPL;
     named_arrive(kBarSFree + 0, kAll);  // both S buffers start free
     named_arrive(kBarSFree + 1, kAll);
@@ -480,10 +487,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 #pragma unroll
       for (int k = 0; k < ROWS; ++k) {
         if (k < ROWS - 1 || rw + k * kWsRowWarps < nloc) {
-          const unsigned char* a = base + k * (kWsRowWarps * kRowBytes);
+          const unsigned char* a = base + k * (kWsRowWarps * RB);
           float fv[EPL];
           double v[EPL];
-          if constexpr (sizeof(T) == 4) {
+          if constexpr (sizeof(T) == 4 && EPL == 4) {
+            const float4 f = *reinterpret_cast<const float4*>(a);
+            fv[0] = f.x; fv[1] = f.y; fv[2] = f.z; fv[3] = f.w;
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) v[e] = fv[e];
+          } else if constexpr (sizeof(T) == 4) {
             const float2 f = *reinterpret_cast<const float2*>(a);
             fv[0] = f.x; fv[EPL - 1] = f.y;
             v[0] = f.x; v[EPL - 1] = f.y;
@@ -605,6 +617,29 @@ int launch_ws(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStrea
   }
   if (!pl.ext) sp.groups = pl.grid;  // ext: the caller sets the slice groups
   const int rows = (int)(((pl.ext ? pl.rpc : sp.n) + rw - 1) / rw);
+  if constexpr (sizeof(T) == 4) {
+    if (pl.rb == 512 && !pl.ext) {  // wide rows (make_plan: fp32, n <= ~210)
+      switch (sp.mode * 32 + rows) {
+#define PIDB_WR_CASE(M, R) \
+  case M * 32 + R: return launch(rows_ws_kernel<float, R, M, false, 512>, tm, sp, pl, st);
+#define PIDB_WR_MODE(M)                                                                   \
+  PIDB_WR_CASE(M, 1) PIDB_WR_CASE(M, 2) PIDB_WR_CASE(M, 3) PIDB_WR_CASE(M, 4)             \
+  PIDB_WR_CASE(M, 5) PIDB_WR_CASE(M, 6) PIDB_WR_CASE(M, 7) PIDB_WR_CASE(M, 8)             \
+  PIDB_WR_CASE(M, 9) PIDB_WR_CASE(M, 10) PIDB_WR_CASE(M, 11) PIDB_WR_CASE(M, 12)          \
+  PIDB_WR_CASE(M, 13) PIDB_WR_CASE(M, 14) PIDB_WR_CASE(M, 15) PIDB_WR_CASE(M, 16)         \
+  PIDB_WR_CASE(M, 17) PIDB_WR_CASE(M, 18)
+        PIDB_WR_MODE(0) PIDB_WR_MODE(1) PIDB_WR_MODE(3)
+        PIDB_WR_CASE(1, 19) PIDB_WR_CASE(1, 20) PIDB_WR_CASE(1, 21) PIDB_WR_CASE(1, 22)
+        PIDB_WR_CASE(1, 23) PIDB_WR_CASE(1, 24) PIDB_WR_CASE(1, 25) PIDB_WR_CASE(1, 26)
+        PIDB_WR_CASE(1, 27)
+#undef PIDB_WR_MODE
+#undef PIDB_WR_CASE
+        default:
+          set_error("no wide-row kernel for %d rows per warp", rows);
+          return PIDB_EUNSUPPORTED;
+      }
+    }
+  }
   switch (sp.mode * 32 + rows) {
 #define PIDB_WS_CASE(M, R) \
   case M * 32 + R: return launch(rows_ws_kernel<T, R, M, false>, tm, sp, pl, st);

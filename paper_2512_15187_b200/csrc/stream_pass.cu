@@ -506,6 +506,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---------------------------------------------------------------- host side
 
+// SMEM tail of rows_ws_kernel (single CTA): barriers, sS/sW[2][V], the
+// column group's red[<= 8 warps][V], ticket and per-warp column sums
+size_t ws_tail(int V) {
+  return 128 + (size_t)4 * V * 8 + (size_t)8 * V * 8 + 16 + kRowsWarps * 8 + 64;
+}
 size_t rows_tail(int V, int cs) {
   return 128 + (size_t)4 * V * 8 + (size_t)2 * kRowsWarps * V * 8 + 16 + kRowsWarps * 8 + 64 +
          (cs > 1 ? (size_t)4 * cs * V * 8 + 16 : 0);
@@ -568,6 +573,31 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl, int mode = MODE_MEAN) 
       }
       pl.cs = 1;
       pl.rpc = (int)n;
+    }
+  }
+  if (n <= 256 && esize == 4 && ws_eligible(mode) && std::getenv("PIDB_WS") == nullptr &&
+      !(std::getenv("PIDB_RB") && std::atoi(std::getenv("PIDB_RB")) == 256)) {
+    // wide rows: 512-byte member-row segments per tile (HBM streams them
+    // faster than 256-byte ones, profiles/r02_ubench_rows.log) when three
+    // stages of n rows fit (n <= 142): K5 n = 64 / 100 / 140 x 512^3
+    // 8.54 / 10.60 / 13.05 -> 7.63 / 9.52 / 11.43 ms; with only two stages
+    // (n = 200) the ring runs dry: 15.4 -> 16.0 ms, so 256-byte rows stay
+    // (profiles/r02_k5_wide_rows.txt).  Warp-specialised kernel only.
+    constexpr int RB = 512, V2 = RB / 4;
+    const uint32_t sb = (uint32_t)align_up((size_t)n * RB, 1024);
+    const size_t tb = ws_tail(V2) + 1024;
+    const int st = (int)std::min<size_t>(kMaxStages, (kSmemBudget - tb) / sb);
+    if (st >= 3) {
+      pl.chunked = false;
+      pl.rb = RB;
+      pl.tiles = (m + V2 - 1) / V2;
+      pl.grid = (int)std::min<int64_t>(pl.tiles, sm_count());
+      pl.rows = (int)((n + kRowsWarps - 1) / kRowsWarps);
+      pl.box_rows = (int)n;
+      pl.stage_bytes = sb;
+      pl.stages = st;
+      pl.smem = (size_t)st * sb + tb;
+      return true;
     }
   }
   if (n <= 256) {
@@ -751,7 +781,7 @@ int run_stream_pass(int mode, const void* u, int dtype, int64_t n, int64_t m, in
   int rc = encode_tma_2d(&tm, u,
                          dtype == PIDB_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
-                         (uint64_t)m, (uint64_t)n, (uint64_t)ld * es, (uint32_t)(kRowBytes / es),
+                         (uint64_t)m, (uint64_t)n, (uint64_t)ld * es, (uint32_t)(pl.rb / es),
                          (uint32_t)pl.box_rows, CU_TENSOR_MAP_SWIZZLE_NONE);
   if (rc != PIDB_OK) return rc;
   char* base = static_cast<char*>(ws);
