@@ -309,7 +309,7 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
 template <typename T, int ROWS, int MODE, bool CL, int RB = kRowBytes>
 __global__ void __launch_bounds__(kRowsThreads, 1)
     rows_ws_kernel(const __grid_constant__ CUtensorMap tmap, const StreamParams p) {
-  static_assert(RB == kRowBytes || (!CL && sizeof(T) == 4), "wide rows: fp32, single CTA");
+  static_assert(RB == kRowBytes || !CL, "wide rows: single-CTA kernel only");
   constexpr int kWsColWarps = ws_col_warps(MODE);
   constexpr int kWsColThreads = kWsColWarps * 32;
   constexpr int kWsRowWarps = kRowsWarps - kWsColWarps;
@@ -499,6 +499,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             const float2 f = *reinterpret_cast<const float2*>(a);
             fv[0] = f.x; fv[EPL - 1] = f.y;
             v[0] = f.x; v[EPL - 1] = f.y;
+          } else if constexpr (EPL == 2) {
+            const double2 f = *reinterpret_cast<const double2*>(a);
+            v[0] = f.x; v[1] = f.y;
+            fv[0] = fv[1] = 0.f;
           } else {
             v[0] = *reinterpret_cast<const double*>(a);
             fv[0] = 0.f;
@@ -617,11 +621,11 @@ int launch_ws(const CUtensorMap& tm, StreamParams& sp, const Plan& pl, cudaStrea
   }
   if (!pl.ext) sp.groups = pl.grid;  // ext: the caller sets the slice groups
   const int rows = (int)(((pl.ext ? pl.rpc : sp.n) + rw - 1) / rw);
-  if constexpr (sizeof(T) == 4) {
-    if (pl.rb == 512 && !pl.ext) {  // wide rows (make_plan: fp32, n <= ~210)
+  {
+    if (pl.rb == 512 && !pl.ext) {  // wide rows (make_plan: n <= 142)
       switch (sp.mode * 32 + rows) {
 #define PIDB_WR_CASE(M, R) \
-  case M * 32 + R: return launch(rows_ws_kernel<float, R, M, false, 512>, tm, sp, pl, st);
+  case M * 32 + R: return launch(rows_ws_kernel<T, R, M, false, 512>, tm, sp, pl, st);
 #define PIDB_WR_MODE(M)                                                                   \
   PIDB_WR_CASE(M, 1) PIDB_WR_CASE(M, 2) PIDB_WR_CASE(M, 3) PIDB_WR_CASE(M, 4)             \
   PIDB_WR_CASE(M, 5) PIDB_WR_CASE(M, 6) PIDB_WR_CASE(M, 7) PIDB_WR_CASE(M, 8)             \

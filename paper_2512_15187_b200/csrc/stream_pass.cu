@@ -575,7 +575,7 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl, int mode = MODE_MEAN) 
       pl.rpc = (int)n;
     }
   }
-  if (n <= 256 && esize == 4 && ws_eligible(mode) && std::getenv("PIDB_WS") == nullptr &&
+  if (n <= 256 && ws_eligible(mode) && std::getenv("PIDB_WS") == nullptr &&
       !(std::getenv("PIDB_RB") && std::atoi(std::getenv("PIDB_RB")) == 256)) {
     // wide rows: 512-byte member-row segments per tile (HBM streams them
     // faster than 256-byte ones, profiles/r02_ubench_rows.log) when three
@@ -583,7 +583,8 @@ bool make_plan(int64_t n, int64_t m, int esize, Plan& pl, int mode = MODE_MEAN) 
     // 8.54 / 10.60 / 13.05 -> 7.63 / 9.52 / 11.43 ms; with only two stages
     // (n = 200) the ring runs dry: 15.4 -> 16.0 ms, so 256-byte rows stay
     // (profiles/r02_k5_wide_rows.txt).  Warp-specialised kernel only.
-    constexpr int RB = 512, V2 = RB / 4;
+    constexpr int RB = 512;
+    const int V2 = RB / esize;
     const uint32_t sb = (uint32_t)align_up((size_t)n * RB, 1024);
     const size_t tb = ws_tail(V2) + 1024;
     const int st = (int)std::min<size_t>(kMaxStages, (kSmemBudget - tb) / sb);
