@@ -2,7 +2,8 @@
 (memcheck / racecheck / synccheck; tools/sanitize.sh) and as a crash sweep:
 K5/K9 rows (WS and plain), cluster WS, chunked, wide/ext (n > 4096), fp64
 members, K6 masses, similarity, K7 pack + K2 i8 Gram + exact epilogue, the
-tensor-core PID Gram (fused sums) and the full Gram, the fp64 gram_block
+tensor-core PID Gram (fused sums) and the full Gram, byte-ensemble eID
+(K7 count-only + K2 from the bytes), the fp64 gram_block
 seam, K8 pair sums, mean mask, validation, K10 band envelopes.
 ``--quick`` keeps one case per variant (racecheck is slow)."""
 import sys
@@ -38,7 +39,11 @@ r = pb.depth_eid(de)
 pb.depth_pid(de, algorithm="gram")
 reduction.gram_device(de)
 pb.boxplot.band_envelopes(de, r.rank, [13, 65, 130], 0.5)
-print("ok eid/gram/boxplot", flush=True)
+for nb, mb in ((130, 1000), (257, 129), (3, 17)):  # byte ensembles: K7 count-only + K2 by TMA
+    Bb = rng.uniform(size=(nb, mb)) < 0.5
+    pb.depth_eid(torch.from_numpy(Bb))
+    pb.depth_eid(torch.from_numpy(Bb.astype(np.uint8)))
+print("ok eid/gram/boxplot/bytes", flush=True)
 a = rng.uniform(size=(37, 1001))
 b = rng.uniform(size=(70, 1001)).astype(np.float32)
 reduction.gram_block(a, b, rng.uniform(0.5, 2, size=1001), complement_cols=True)
