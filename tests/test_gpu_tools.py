@@ -108,6 +108,14 @@ def test_stage_manifest_binary_is_byte_ensemble(pb, tmp_path):
     for fn in (pb.depth_eid, pb.depth_pid, pb.depth_pid_mean):
         a, b = fn(de), fn(e)
         assert np.array_equal(a.depth, b.depth) and np.array_equal(a.rank, b.rank)
+    from paper_2512_15187_b200.cli import main as cli_main
+
+    for meth in ("eid", "pid", "pid-mean"):  # the CLI on the byte ensemble
+        out = tmp_path / f"d_{meth}.csv"
+        assert cli_main(["depth", "--manifest", str(tmp_path / "m.json"), "--method", meth,
+                         "--out", str(out)]) == 0
+        got = pb.read_depth_csv(out)
+        assert np.array_equal(got.depth, pb.depth_by_method(e, meth).depth)
     bad = (rng.uniform(size=(9, 11)) < 0.5).astype(np.uint8) * 2
     pb.write_volume(bad, tmp_path / "v/bad.npy")
     pb.write_manifest(tmp_path / "bad.json", (9, 11), entries + [{"id": "two", "path": "v/bad.npy"}])
