@@ -23,27 +23,34 @@
 //            int32 accumulators in TMEM (exact: < 2^31 cells per pair)
 //   warps 2-5: epilogue, tcgen05.ld 32x32b -> int32 split partials
 // A second kernel sums the split partials in int64 and mirrors the triangle.
+#include <cstdlib>
+
 #include "tcgen05.cuh"
 
 namespace pidb {
 namespace {
 
-constexpr int kBM = 128, kBN = 256, kBK = 128;  // bytes of K per stage
+// H = 128-member halves of the B panel: H = 2 -> 128 x 256 output tiles,
+// H = 1 -> 128 x 128 (more, smaller tiles for small n; plan_i8 picks)
+constexpr int kBM = 128, kBK = 128;  // kBK: bytes of K per stage
 constexpr int kStages = 4;
-constexpr int kABytes = kBM * kBK, kBBytes = kBN * kBK;
-constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kABytes = kBM * kBK;
+template <int H> constexpr int kBNh = 128 * H;
+template <int H> constexpr int kStageBytesH = kABytes * (1 + H);
 constexpr int kGramThreads = 192;
-constexpr uint32_t kIdescI8 = tc::idesc(tc::kCS32, tc::kU8, kBM, kBN);
+template <int H>
+constexpr uint32_t kIdescH = tc::idesc(tc::kCS32, tc::kU8, kBM, 128 * H);
 
 struct GramI8Params {
   int n, nib, njb, ntiles, splits, kblocks, kb_per;
-  int32_t* part;  // [units][kBM][kBN]
+  int32_t* part;  // [units][kBM][BN]
 };
 
+template <int H>
 __device__ __forceinline__ void tile_of(int t, int nib, int& ib, int& jb) {
   jb = 0;
   for (;;) {
-    const int c = min(nib, 2 * jb + 2);
+    const int c = min(nib, H * (jb + 1));
     if (t < c) break;
     t -= c;
     ++jb;
@@ -51,10 +58,11 @@ __device__ __forceinline__ void tile_of(int t, int nib, int& ib, int& jb) {
   ib = t;
 }
 
-template <bool kBytes>
+template <bool kBytes, int H>
 __global__ void __launch_bounds__(kGramThreads, 1)
     gram_i8_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ tiles,
                    const GramI8Params p) {
+  constexpr int kBN = kBNh<H>, kStageBytes = kStageBytesH<H>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   unsigned char* ring = smem_raw + pad;
@@ -67,7 +75,7 @@ __global__ void __launch_bounds__(kGramThreads, 1)
   const int unit = blockIdx.x;
   const int t = unit / p.splits, split = unit - t * p.splits;
   int ib, jb;
-  tile_of(t, p.nib, ib, jb);
+  tile_of<H>(t, p.nib, ib, jb);
   const int kb0 = split * p.kb_per;
   const int kb1 = min(p.kblocks, kb0 + p.kb_per);
   const int nk = max(0, kb1 - kb0);
@@ -96,21 +104,23 @@ __global__ void __launch_bounds__(kGramThreads, 1)
         mbar_wait(&empty[s], ph ^ 1u);
         unsigned char* a = ring + s * kStageBytes;
         mbar_arrive_expect_tx(&full[s], kStageBytes);
-        const int64_t kb = kb0 + k;  // three 16 KB tiles: A, then B's two halves
+        const int64_t kb = kb0 + k;  // 16 KB tiles: A, then the H halves of B
         PIDB_DCHECK(kb < p.kblocks && ib < 2 * ((p.n + 255) / 256) &&
-                        2 * jb + 1 < 2 * ((p.n + 255) / 256),
+                        H * jb + H - 1 < 2 * ((p.n + 255) / 256),
                     "K2 operand tile bounds");
         if constexpr (kBytes) {
           const int32_t x = (int32_t)(kb * kBK);
           tma_load_2d(a, &tmap, x, ib * kBM, &full[s], pol);
-          tma_load_2d(a + kABytes, &tmap, x, 2 * jb * kBM, &full[s], pol);
-          tma_load_2d(a + 2 * kABytes, &tmap, x, (2 * jb + 1) * kBM, &full[s], pol);
+#pragma unroll
+          for (int h = 0; h < H; ++h)
+            tma_load_2d(a + (1 + h) * kABytes, &tmap, x, (H * jb + h) * kBM, &full[s], pol);
         } else {
           bulk_load(a, tiles + ((int64_t)ib * p.kblocks + kb) * kABytes, kABytes, &full[s], pol);
-          bulk_load(a + kABytes, tiles + ((int64_t)(2 * jb) * p.kblocks + kb) * kABytes, kABytes,
-                    &full[s], pol);
-          bulk_load(a + 2 * kABytes, tiles + ((int64_t)(2 * jb + 1) * p.kblocks + kb) * kABytes,
-                    kABytes, &full[s], pol);
+#pragma unroll
+          for (int h = 0; h < H; ++h)
+            bulk_load(a + (1 + h) * kABytes,
+                      tiles + ((int64_t)(H * jb + h) * p.kblocks + kb) * kABytes, kABytes,
+                      &full[s], pol);
         }
         if (++s == kStages) { s = 0; ph ^= 1u; }
       }
@@ -127,7 +137,7 @@ __global__ void __launch_bounds__(kGramThreads, 1)
         const uint64_t db = tc::desc_kmajor_sw128(a + kABytes);
 #pragma unroll
         for (int kk = 0; kk < kBK / 32; ++kk)  // K = 32 bytes per MMA
-          tc::mma_i8(tmem, da + 2 * kk, db + 2 * kk, kIdescI8, (k | kk) != 0);
+          tc::mma_i8(tmem, da + 2 * kk, db + 2 * kk, kIdescH<H>, (k | kk) != 0);
         tc::commit(&empty[s]);  // frees the stage once these MMAs are done
         if (++s == kStages) { s = 0; ph ^= 1u; }
       }
@@ -165,14 +175,17 @@ __global__ void __launch_bounds__(kGramThreads, 1)
 // One thread per (tile, tile row, 4 consecutive columns): 16-byte partial
 // loads along the row (coalesced), int64 sums (exact, any order), the upper
 // entries written along the row and mirrored into the lower triangle.
+template <int H>
 __global__ void __launch_bounds__(256)
     gram_i8_reduce_kernel(const int32_t* __restrict__ part, int n, int nib, int splits,
                           int64_t* __restrict__ out) {
-  const int t = blockIdx.x >> 5;                      // tile
-  const int r = ((blockIdx.x & 31) << 2) + (threadIdx.x >> 6);  // tile row 0..127
-  const int c4 = (threadIdx.x & 63) << 2;             // first of 4 tile columns
+  constexpr int kBN = kBNh<H>;
+  constexpr int TPR = kBN / 4, RPB = 256 / TPR, BPT = kBM / RPB;  // threads/row, rows/block
+  const int t = blockIdx.x / BPT;                                    // tile
+  const int r = (blockIdx.x % BPT) * RPB + threadIdx.x / TPR;        // tile row 0..127
+  const int c4 = (threadIdx.x % TPR) * 4;                            // first of 4 tile columns
   int ib, jb;
-  tile_of(t, nib, ib, jb);
+  tile_of<H>(t, nib, ib, jb);
   const int i = ib * kBM + r, j0 = jb * kBN + c4;
   if (i >= n || j0 >= n || j0 + 3 < i) return;
   const int4* src = reinterpret_cast<const int4*>(part + ((size_t)t * splits * kBM + r) * kBN + c4);
@@ -192,39 +205,64 @@ __global__ void __launch_bounds__(256)
 }
 
 struct GramPlan {
-  int nib, njb, ntiles, splits, kblocks, kb_per, units;
+  int h, nib, njb, ntiles, splits, kblocks, kb_per, units;
   size_t smem, ws;
 };
 
+// Tile shape (H) and K splits minimising the makespan, in cycles per SM:
+// waves x (K blocks per unit x ~256 (1 + H) cycles -- a K block is operand-
+// delivery paced, (1 + H) 16 KB tiles into SMEM, not MMA paced (256 H) --
+// + ~5000 cycles of per-unit cost: TMEM alloc, pipeline fill, the int32
+// partial tile).  Measured (byte ensembles, 512^2 cells): 128 x 128 tiles
+// win only for n <= 256 (n = 250: 0.049 vs 0.057 ms); n = 500 / 1000 / 1500
+// / 4000: 128 x 256 tiles 0.066 / 0.134 / 0.258 / 1.457 ms vs 0.074 / 0.174
+// / 0.590 / 2.510 ms (PIDB_K2_H forces a shape).
 GramPlan plan_i8(int64_t n, int64_t m) {
-  GramPlan g{};
-  g.nib = (int)((n + kBM - 1) / kBM);
-  g.njb = (int)((n + kBN - 1) / kBN);
-  g.ntiles = 0;
-  for (int jb = 0; jb < g.njb; ++jb) g.ntiles += std::min(g.nib, 2 * jb + 2);
-  g.kblocks = (int)((m + kBK - 1) / kBK);
+  GramPlan best{};
+  long best_cost = -1;
   const int sms = sm_count();
-  // K splits minimising the makespan: waves x (K blocks per unit + a fixed
-  // per-unit cost of ~10 K blocks: TMEM alloc, pipeline fill, the 128 KB
-  // partial).  One wave when it divides well (n = 500: 6 tiles x 24 splits);
-  // n = 1500: 42 tiles x 7 splits in two waves (586 K blocks per SM) over
-  // 3 splits in one wave (683, 22 SMs idle) -- measured 0.258 vs 0.264 ms:
-  // the lock-step waves keep K2 tensor/L2-paced, not occupancy-paced.
-  {
-    long best = -1;
-    const int smax = std::max(1, std::min(g.kblocks, 8 * sms / g.ntiles + 1));
+  const int kblocks = (int)((m + kBK - 1) / kBK);
+  for (int h = 1; h <= 2; ++h) {
+    GramPlan g{};
+    g.h = h;
+    g.nib = (int)((n + kBM - 1) / kBM);
+    g.njb = (int)((n + 128 * h - 1) / (128 * h));
+    g.ntiles = 0;
+    for (int jb = 0; jb < g.njb; ++jb) g.ntiles += std::min(g.nib, h * (jb + 1));
+    g.kblocks = kblocks;
+    const int smax = std::max(1, std::min(kblocks, 8 * sms / g.ntiles + 1));
     for (int s = 1; s <= smax; ++s) {
-      const int per = (g.kblocks + s - 1) / s;
-      const int sp = (g.kblocks + per - 1) / per;
+      const int per = (kblocks + s - 1) / s;
+      const int sp = (kblocks + per - 1) / per;
       const long waves = ((long)g.ntiles * sp + sms - 1) / sms;
-      const long cost = waves * (per + 10);
-      if (best < 0 || cost < best) { best = cost; g.splits = sp; g.kb_per = per; }
+      const long cost = waves * ((long)per * 256 * (1 + h) + 5000);
+      if (best_cost < 0 || cost < best_cost) {
+        best_cost = cost;
+        g.splits = sp;
+        g.kb_per = per;
+        best = g;
+      }
     }
   }
-  g.units = g.ntiles * g.splits;
-  g.smem = 1024 + (size_t)kStages * kStageBytes + 256;
-  g.ws = 256 + (size_t)g.units * kBM * kBN * sizeof(int32_t);
-  return g;
+  if (const char* e = std::getenv("PIDB_K2_H")) {  // A/B: force the tile shape
+    const int want = std::atoi(e);
+    if (want != best.h && (want == 1 || want == 2)) {
+      GramPlan g{};
+      g.h = want;
+      g.nib = (int)((n + kBM - 1) / kBM);
+      g.njb = (int)((n + 128 * want - 1) / (128 * want));
+      for (int jb = 0; jb < g.njb; ++jb) g.ntiles += std::min(g.nib, want * (jb + 1));
+      g.kblocks = kblocks;
+      g.splits = std::max(1, std::min(kblocks, sms / g.ntiles));
+      g.kb_per = (kblocks + g.splits - 1) / g.splits;
+      g.splits = (kblocks + g.kb_per - 1) / g.kb_per;
+      best = g;
+    }
+  }
+  best.units = best.ntiles * best.splits;
+  best.smem = 1024 + (size_t)kStages * kABytes * (1 + best.h) + 256;
+  best.ws = 256 + (size_t)best.units * kBM * 128 * best.h * sizeof(int32_t);
+  return best;
 }
 
 }  // namespace
@@ -237,21 +275,29 @@ extern "C" size_t pidb_gram_i8_workspace_bytes(int64_t n, int64_t m) {
   return plan_i8(n, m).ws;
 }
 
-static int launch_i8(const CUtensorMap& tmap, const uint8_t* tiles, bool bytes, int64_t n,
-                     int64_t m, int64_t* gram, void* ws, size_t ws_bytes, cudaStream_t st) {
-  const GramPlan g = plan_i8(n, m);
-  PIDB_REQUIRE(ws && ws_bytes >= g.ws, "workspace too small: need %zu bytes", g.ws);
+template <int H>
+static int launch_i8_h(const CUtensorMap& tmap, const uint8_t* tiles, bool bytes,
+                       const GramPlan& g, int64_t n, int64_t* gram, void* ws, cudaStream_t st) {
   GramI8Params p{};
   p.n = (int)n; p.nib = g.nib; p.njb = g.njb; p.ntiles = g.ntiles; p.splits = g.splits;
   p.kblocks = g.kblocks; p.kb_per = g.kb_per;
   p.part = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + 256);
-  auto kern = bytes ? gram_i8_kernel<true> : gram_i8_kernel<false>;
+  auto kern = bytes ? gram_i8_kernel<true, H> : gram_i8_kernel<false, H>;
   PIDB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
   kern<<<g.units, kGramThreads, g.smem, st>>>(tmap, tiles, p);
   PIDB_LAUNCH_CHECK("gram_i8_kernel");
-  gram_i8_reduce_kernel<<<g.ntiles * 32, 256, 0, st>>>(p.part, (int)n, g.nib, g.splits, gram);
+  constexpr int BPT = kBM / (256 / (kBNh<H> / 4));
+  gram_i8_reduce_kernel<H><<<g.ntiles * BPT, 256, 0, st>>>(p.part, (int)n, g.nib, g.splits, gram);
   PIDB_LAUNCH_CHECK("gram_i8_reduce_kernel");
   return PIDB_OK;
+}
+
+static int launch_i8(const CUtensorMap& tmap, const uint8_t* tiles, bool bytes, int64_t n,
+                     int64_t m, int64_t* gram, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const GramPlan g = plan_i8(n, m);
+  PIDB_REQUIRE(ws && ws_bytes >= g.ws, "workspace too small: need %zu bytes", g.ws);
+  return g.h == 1 ? launch_i8_h<1>(tmap, tiles, bytes, g, n, gram, ws, st)
+                  : launch_i8_h<2>(tmap, tiles, bytes, g, n, gram, ws, st);
 }
 
 extern "C" int pidb_gram_i8(const uint8_t* tiles, int64_t n, int64_t m, int64_t* gram, void* ws,
